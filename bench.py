@@ -1,0 +1,361 @@
+"""msGeMM benchmark (driver contract: one JSON line from rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg5] [--impl ours|reference]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...
+
+Workload (default): BASELINE.json config 5 -- W 65536x8192 int4, X 8192x8
+fp16 ~N(0,1), d=3 -- the configuration the metric's "1/2/4/8 B200" refers to
+and the largest single-GPU one.  At N GPUs the 65536 rows are sharded over
+the ranks (strong scaling: total work fixed) and the Y slices are
+all-gathered with NCCL.  A "step" is one full msGeMM of the config.
+
+Metric: effective GOP/s = 2*m*k*b / step time (whole job), plus the HBM
+roofline of the dominant kernel (fused LUT kernel) and end-to-end numbers
+through the public API with pinned host buffers.  L2 reuse across steps is
+defeated by rotating over >= 3x L2 worth of distinct weight copies.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+from paper_2310_06178_b200.workloads import CONFIGS, algorithmic_bytes, effective_ops  # noqa: E402
+
+L2_BYTES = 126 * 1024 * 1024
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)",
+                "sm_max_mhz": d.get("sm_max_mhz")}
+    return dict(PEAKS_FALLBACK)
+
+
+# --------------------------------------------------------------------------- clocks
+_REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+            0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+            0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+            0x100: "display_clock_setting"}
+
+
+class ClockSampler(threading.Thread):
+    """Samples SM clock and throttle reasons via NVML while the timed region runs."""
+
+    def __init__(self, torch_dev):
+        super().__init__(daemon=True)
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._halt = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            uuid = str(torch.cuda.get_device_properties(torch_dev).uuid)
+            uuid = uuid if uuid.startswith("GPU-") else "GPU-" + uuid
+            self.h = pynvml.nvmlDeviceGetHandleByUUID(uuid.encode())
+            self.nv = pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - reported in the JSON
+            self.err = repr(e)
+
+    def sample(self):
+        if not self.ok:
+            return
+        nv = self.nv
+        self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+        mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        for bit, name in _REASONS.items():
+            if mask & bit:
+                self.reasons.add(name)
+
+    def run(self):
+        while not self._halt.is_set():
+            self.sample()
+            time.sleep(0.005)
+
+    def stop(self):
+        self._halt.set()
+        self.join(timeout=1)
+        self.sample()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": self.err}
+        return {"sm_mhz": float(statistics.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "samples": len(self.samples),
+                "reasons": sorted(self.reasons - {"gpu_idle"})}
+
+
+# --------------------------------------------------------------------------- CPU baseline
+class CpuArm:
+    """The oracle port (numpy restatement of the reference's msgemm) on row
+    samples of the same workload, host threads across batch columns (the
+    reference's own ThreadPool split, gemm.py:136-152)."""
+
+    def __init__(self, cfg):
+        from oracle import msgemm_oracle as orc
+        from paper_2310_06178_b200.workloads import activations, weights
+        self.orc, self.cfg = orc, cfg
+        self.data = weights(cfg)
+        X = activations(cfg)
+        self.X = X.astype(np.int64) if cfg.x_dtype == "int" else X
+        self.cores = min(len(os.sched_getaffinity(0)), max(cfg.b, 1))
+        self.vals = orc.int4_values()
+
+    def run(self, r0, rows):
+        cfg = self.cfg
+        r0 = r0 % max(cfg.m - rows + 1, 1)
+        t0 = time.perf_counter()
+        self.orc.msgemm(self.data[r0:r0 + rows], rows, cfg.k, 4, self.vals, self.X, cfg.d,
+                        workers=self.cores)
+        return time.perf_counter() - t0
+
+    def rows_for(self, target_s):
+        rows = min(self.cfg.m, 256)
+        t = self.run(0, rows)
+        return int(min(self.cfg.m, max(16, rows * target_s / max(t, 1e-4))))
+
+    def gops(self, rows, seconds):
+        return 2.0 * rows * self.cfg.k * self.cfg.b / seconds / 1e9
+
+    def describe(self, rows, seconds, nsteps=1):
+        cfg = self.cfg
+        return (f"oracle port (numpy, reference algorithm) on {nsteps} x {rows} rows of "
+                f"{cfg.m} (k={cfg.k}, b={cfg.b}, d={cfg.d}), workers={self.cores}, "
+                f"{seconds:.2f}s total")
+
+
+def cpu_baseline(cfg, target_s: float = 10.0):
+    arm = CpuArm(cfg)
+    rows = arm.rows_for(target_s)
+    t = arm.run(0, rows)
+    return {"value": arm.gops(rows, t), "unit": "GOP/s", "cores": arm.cores, "kind": "port",
+            "sample": arm.describe(rows, t)}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU algorithm (oracle port) on this host,
+    each step a bounded row sample; the whole run stays within a few minutes."""
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    arm = CpuArm(cfg)
+    per_step = min(5.0, max(0.05, 120.0 / max(args.steps + args.warmup, 1)))
+    rows = arm.rows_for(per_step)
+    for i in range(args.warmup):
+        arm.run(i * rows, rows)
+    total = 0.0
+    for i in range(args.steps):
+        total += arm.run((args.warmup + i) * rows, rows)
+    value = arm.gops(rows * args.steps, total)
+    out = {
+        "metric": "effective GOP/s (2*m*k*b/time) and achieved HBM GB/s vs roofline",
+        "value": value, "unit": "GOP/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f16" if cfg.x_dtype == "float16"
+        else cfg.x_dtype, "data": "synthetic (seeded numpy default_rng)", "impl": "reference",
+        "config": {"workload": cfg.name, "m": cfg.m, "k": cfg.k, "b": cfg.b, "d": cfg.d,
+                   "step": f"{rows}-row sample of the workload"},
+        "cpu_baseline": {"value": value, "unit": "GOP/s", "cores": arm.cores, "kind": "port",
+                         "sample": arm.describe(rows, total, args.steps)},
+        "e2e": {"value": value, "unit": "GOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="cfg5", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2310_06178_b200 as mg
+    from paper_2310_06178_b200 import _lib
+    from paper_2310_06178_b200.workloads import activations, weights
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = CONFIGS[args.config]
+    if cfg.m % world:
+        raise SystemExit(f"m={cfg.m} not divisible by {world} ranks")
+    mr = cfg.m // world
+    r0 = rank * mr
+
+    data = weights(cfg)[r0:r0 + mr]
+    X = activations(cfg)
+    exact = cfg.x_dtype == "int"
+    Xh = X.astype(np.float16) if exact else X
+    xd = torch.from_numpy(Xh).to(dev)
+    kw = dict(table_dtype=np.float32, out_dtype=np.float32) if exact else {}
+    y_dt = torch.float32 if exact else xd.dtype
+
+    # distinct weight copies so consecutive steps never hit in L2
+    shard_bytes = data.nbytes
+    ncopies = max(2, math.ceil(3 * L2_BYTES / shard_bytes))
+    base = torch.from_numpy(data).to(dev)
+    pwms = []
+    for c in range(ncopies):
+        dd = base if c == 0 else base.clone()
+        pwms.append(mg.PackedWeightMatrix(m=mr, k=cfg.k, width=4, data=dd,
+                                          codebook=mg.int4_codebook()))
+    Yshard = torch.empty((mr, cfg.b), dtype=y_dt, device=dev)
+    Yfull = torch.empty((cfg.m, cfg.b), dtype=y_dt, device=dev) if world > 1 else Yshard
+
+    def step(i, flags=0):
+        mg.msgemm(pwms[i % ncopies], xd, cfg.d, out=Yshard, _flags=flags, **kw)
+        if world > 1 and not flags:
+            dist.all_gather_into_tensor(Yfull, Yshard)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def timed(nsteps, flags=0):
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(nsteps):
+            step(i, flags)
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            tt = torch.tensor([ms], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = tt.item()
+        return ms / nsteps
+
+    for i in range(max(args.warmup, ncopies)):     # also builds every copy's repacked layout
+        step(i)
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(dev)
+    sampler.start()
+    ms_step = timed(args.steps)
+    sampler.stop()
+    clocks = sampler.summary()
+
+    # dominant kernel alone (fused LUT kernel; finish kernel and all-gather skipped)
+    for i in range(3):
+        step(i, _lib.FLAG_LUT_PHASE_ONLY)
+    ms_lut = timed(args.steps, _lib.FLAG_LUT_PHASE_ONLY)
+
+    # end to end through the public API: pinned host X in, host Y out, every step
+    e2e_steps = args.e2e_steps or max(3, min(args.steps, 50))
+    Xpin = torch.from_numpy(Xh).pin_memory()
+    Ypin = torch.empty((cfg.m, cfg.b), dtype=y_dt, pin_memory=True)
+
+    def e2e_step(i):
+        if world == 1:
+            mg.msgemm(pwms[i % ncopies], Xpin, cfg.d, out=Ypin, **kw)
+        else:
+            x_dev = Xpin.to(dev, non_blocking=True)
+            mg.msgemm(pwms[i % ncopies], x_dev, cfg.d, out=Yshard, **kw)
+            dist.all_gather_into_tensor(Yfull, Yshard)
+            Ypin.copy_(Yfull)
+
+    for i in range(3):
+        e2e_step(i)
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(e2e_steps):
+        e2e_step(i)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = 1e3 * (time.perf_counter() - t0) / e2e_steps
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = tt.item()
+
+    ops = effective_ops(cfg)
+    value = ops / (ms_step * 1e-3) / 1e9
+    peaks = load_peaks()
+    shard_cfg = type(cfg)(cfg.name, mr, cfg.k, cfg.b, cfg.d, cfg.x_dtype, cfg.seed)
+    y_item = 4 if exact else 2
+    bytes_launch = algorithmic_bytes(shard_cfg, x_itemsize=2, y_itemsize=y_item)
+    achieved = bytes_launch / (ms_lut * 1e-3) / 1e9
+    traffic = None
+    tp = ROOT / "profiles" / "traffic.json"
+    if tp.exists():
+        traffic = json.loads(tp.read_text()).get(f"{cfg.name}@{world}")
+    nb = cfg.k // cfg.d
+    smem_bytes = (mr * nb + 2048 * nb) * cfg.b * 2          # LUT reads + half-table writes (fp16)
+    out = {
+        "metric": "effective GOP/s (2*m*k*b/time) and achieved HBM GB/s vs roofline",
+        "value": value, "unit": "GOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f16",
+        "data": "synthetic (seeded numpy default_rng; uniform int4 W, N(0,1) X)",
+        "config": {"workload": cfg.name, "m": cfg.m, "k": cfg.k, "b": cfg.b, "d": cfg.d,
+                   "x": "fp16", "tables": "fp16 sign-symmetric half tables (2048/group)",
+                   "accum": "f32", "y": "fp32" if exact else "fp16",
+                   "parallelism": f"row-shard x{world}" + (" + NCCL all-gather" if world > 1 else ""),
+                   "l2": f"rotate {ncopies} weight copies ({ncopies * shard_bytes / 2**20:.0f} MiB "
+                         f">= 3x L2) between steps"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
+                     "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                     "kernel": "fused_lut_kernel", "kernel_ms": ms_lut,
+                     "kernel_share": ms_lut / ms_step, "algorithmic_bytes_per_launch": bytes_launch,
+                     "peak_source": peaks["source"],
+                     "smem_lut_bytes_per_launch": smem_bytes,
+                     "smem_lut_tbs": smem_bytes / (ms_lut * 1e-3) / 1e12},
+        "e2e": {"value": ops / (e2e_ms * 1e-3) / 1e9, "unit": "GOP/s",
+                "ms_per_step": e2e_ms, "h2d_bytes_per_step": Xh.nbytes,
+                "d2h_bytes_per_step": cfg.m * cfg.b * y_item,
+                "path": "msgemm(pwm, pinned host X) -> host Y" if world == 1 else
+                        "H2D X, msgemm shard, NCCL all-gather, D2H Y"},
+        "gpu_launches": 2 * args.steps,
+        "clocks": clocks,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = cpu_baseline(cfg)
+        out["cpu_baseline"] = cb
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,149 @@
+/*
+ * msgemm_b200.h -- C ABI of the B200-native msGeMM hot path.
+ *
+ * The reference (arXiv 2310.06178, /root/reference/pkg/src/msgemm) is a
+ * pure-Python/numpy library with no FFI; its "drop-in boundary" is the Python
+ * function surface re-exported at pkg/src/msgemm/__init__.py:10-92.  Every
+ * entry point below is the device-side replacement of one of those
+ * functions; the Python package paper_2310_06178_b200 binds them with ctypes
+ * and keeps the reference's signatures, dtypes and error behaviour
+ * (INTEGRATION.md shows the binding).
+ *
+ * Conventions
+ *   - All array pointers are DEVICE pointers, caller-owned; the library never
+ *     allocates device memory.  Scratch goes in a caller-provided workspace
+ *     sized by the matching *_workspace_bytes() query.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *     Every call is stream-ordered and never synchronises the host.
+ *   - Codebook values are passed as a HOST array of 2^width doubles (the
+ *     reference's Codebook.values, codebook.py:16-47); they travel in the
+ *     kernel parameter block.
+ *   - Return 0 on success or a negative MSG_ERR_* code; msg_last_error()
+ *     returns a thread-local message.  Python maps the codes to the
+ *     reference's exception types (ValueError, IndexError, TableBudgetError).
+ *   - Arrays are C-contiguous: packed weights (m, row_bytes(k,width)) uint8,
+ *     X (k, b), Y (m, b), LUT entries (num_blocks, 2^(width*d)).
+ */
+#ifndef MSGEMM_B200_H
+#define MSGEMM_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define MSG_API __attribute__((visibility("default")))
+#else
+#define MSG_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define MSG_OK               0
+#define MSG_ERR_VALUE       -1  /* -> ValueError                        */
+#define MSG_ERR_INDEX       -2  /* -> IndexError                        */
+#define MSG_ERR_BUDGET      -3  /* -> TableBudgetError (MemoryError)    */
+#define MSG_ERR_UNSUPPORTED -4  /* -> NotImplementedError (GPU limits)  */
+#define MSG_ERR_CUDA        -5  /* -> RuntimeError                      */
+#define MSG_ERR_WORKSPACE   -6  /* -> ValueError (workspace too small)  */
+
+/* element types */
+#define MSG_F32  0
+#define MSG_F16  1
+#define MSG_F64  2
+#define MSG_I32  3
+#define MSG_I64  4
+#define MSG_U8   5
+#define MSG_I8   6
+#define MSG_I16  7
+#define MSG_BF16 8
+
+/* scale modes (packing.py:21-36 ScaleSpec) */
+#define MSG_SCALE_NONE      0
+#define MSG_SCALE_PER_ROW   1
+#define MSG_SCALE_PER_GROUP 2
+
+/* msg_gemm flags */
+#define MSG_FLAG_F32_ENTRIES   1  /* fp32 table entries even for fp16 X (exact-int mode)  */
+#define MSG_FLAG_NO_SYMMETRY   2  /* full 16^d tables (default: sign-symmetric half tables) */
+#define MSG_FLAG_FORCE_GENERIC 4  /* global-memory table path (any d, width, dtype)        */
+#define MSG_FLAG_LUT_PHASE_ONLY 8 /* measurement: launch only the fused LUT kernel (Y untouched) */
+
+/* weight layouts produced by msg_repack */
+#define MSG_LAYOUT_NONE 0  /* reference row-major nibbles only      */
+#define MSG_LAYOUT_QUAD 1  /* quad planes for the fused LUT kernel  */
+
+MSG_API const char* msg_last_error(void);
+MSG_API int msg_version(void);
+MSG_API int msg_device_sm_count(void);
+
+/* ---------- packing (packing.py) ---------- */
+
+/* codes (m,k) uint8 -> packed (m,row_bytes) ; packing.py:99-114 _pack_code_rows */
+MSG_API int msg_pack_codes(const uint8_t* codes, int64_t m, int64_t k, int width,
+                   uint8_t* packed, void* stream);
+
+/* packed -> codes (m,k) uint8 ; packing.py:117-128 _unpack_code_rows / :172-174 codes */
+MSG_API int msg_unpack_codes(const uint8_t* packed, int64_t m, int64_t k, int width,
+                     uint8_t* codes, void* stream);
+
+/* packed -> int64 (m, k/d) group indices ; packing.py:219-228 group_indices */
+MSG_API int msg_group_indices(const uint8_t* packed, int64_t m, int64_t k, int width, int d,
+                      int64_t* out, void* stream);
+
+/* values (m,k) of dtype -> packed codes by nearest codebook value, after
+ * dividing out per-element scale grid (optional, same dtype as values, f64);
+ * bad_count receives the number of non-representable weights (device int64)
+ * and bad_first the flat index of the first one.  packing.py:146-169 pack */
+MSG_API int msg_encode_values(const double* weights, const double* grid, int64_t m, int64_t k,
+                      int width, const double* values,
+                      uint8_t* packed, int64_t* bad_count_and_first, void* stream);
+
+/* ---------- phase 1 (lut.py) ---------- */
+
+/* Full table for one activation vector x (k,) with stride `ldx` elements:
+ * entries (k/d, 2^(width*d)) of dtype; built with the reference's rounding
+ * order (lut.py:59-72).  lut.py:98-127 build_lut / :88-95 build_lut_block
+ * (block_lo/block_hi select a block range). */
+MSG_API int msg_lut_build(const void* x, int dtype, int64_t k, int64_t ldx, int d,
+                  const double* values, int width, int64_t block_lo, int64_t block_hi,
+                  void* entries, void* stream);
+
+/* ---------- K3: weight repack ---------- */
+MSG_API int64_t msg_repacked_bytes(int64_t m, int64_t k, int d, int layout);
+/* symmetric=1 folds the sign symmetry of an antisymmetric codebook into the
+ * stored indices (top index bit -> complement + sign bit). */
+MSG_API int msg_repack(const uint8_t* packed, int64_t m, int64_t k, int d, int layout,
+               int symmetric, uint8_t* out, void* stream);
+
+/* ---------- K1+K2: msGeMM (gemm.py:89-153) ---------- */
+
+/* Which layout msg_gemm needs for these arguments (MSG_LAYOUT_*), and the
+ * workspace it needs; returns <0 on argument error. */
+MSG_API int msg_gemm_plan(int64_t m, int64_t k, int width, const double* values, int x_dtype,
+                  int64_t b, int d, int scale_mode, int64_t group_size, int flags,
+                  int* layout_out, int* symmetric_out, int64_t* workspace_bytes_out);
+
+/* Y (m,b) = dequant(W) @ X with the two-phase LUT algorithm.
+ * packed: reference layout (always required); wrep: msg_repack output for
+ * the layout msg_gemm_plan returned (may be NULL when that layout is NONE).
+ * q: scales (PerRow (m,), PerGroup (m, k/group_size)) of q_dtype or NULL. */
+MSG_API int msg_gemm(const uint8_t* packed, const uint8_t* wrep, int64_t m, int64_t k, int width,
+             const double* values, const void* x, int x_dtype, int64_t b, int d,
+             int scale_mode, int64_t group_size, const void* q, int q_dtype,
+             void* y, int y_dtype, void* workspace, int64_t workspace_bytes,
+             int flags, void* stream);
+
+/* ---------- K4: dequantise-then-MMA comparison kernel (gemm.py:206-216 naive_gemm) ---------- */
+MSG_API int64_t msg_dequant_mma_workspace_bytes(int64_t m, int64_t k, int64_t b);
+/* int4 (width 4, any codebook whose values are exact in fp16) x fp16 X (k,b) -> fp32 Y (m,b),
+ * tcgen05.mma kind::f16 with fp32 accumulation in TMEM. */
+MSG_API int msg_dequant_mma(const uint8_t* packed, int64_t m, int64_t k, const double* values,
+                    const void* x_f16, int64_t b, float* y, void* workspace,
+                    int64_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MSGEMM_B200_H */

@@ -1,0 +1,195 @@
+"""ctypes binding of the C-ABI library (include/msgemm_b200.h).
+
+This is the only module that touches the shared library.  It fails loudly:
+there is no CPU fallback anywhere in the package -- if the library or a CUDA
+device is missing, every compute entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+import numpy as np
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "_lib" / "libmsgemm_b200.so"
+
+# status codes / enums mirrored from include/msgemm_b200.h
+MSG_OK = 0
+MSG_ERR_VALUE, MSG_ERR_INDEX, MSG_ERR_BUDGET = -1, -2, -3
+MSG_ERR_UNSUPPORTED, MSG_ERR_CUDA, MSG_ERR_WORKSPACE = -4, -5, -6
+F32, F16, F64, I32, I64, U8, I8, I16, BF16 = range(9)
+SCALE_NONE, SCALE_PER_ROW, SCALE_PER_GROUP = 0, 1, 2
+FLAG_F32_ENTRIES, FLAG_NO_SYMMETRY, FLAG_FORCE_GENERIC, FLAG_LUT_PHASE_ONLY = 1, 2, 4, 8
+LAYOUT_NONE, LAYOUT_QUAD = 0, 1
+
+EXPORTS = (
+    "msg_last_error", "msg_version", "msg_device_sm_count", "msg_pack_codes",
+    "msg_unpack_codes", "msg_group_indices", "msg_encode_values", "msg_lut_build",
+    "msg_repacked_bytes", "msg_repack", "msg_gemm_plan", "msg_gemm",
+    "msg_dequant_mma_workspace_bytes", "msg_dequant_mma",
+)
+
+_c_i64 = ctypes.c_int64
+_c_int = ctypes.c_int
+_vp = ctypes.c_void_p
+_SIGS = {
+    "msg_last_error": (ctypes.c_char_p, []),
+    "msg_version": (_c_int, []),
+    "msg_device_sm_count": (_c_int, []),
+    "msg_pack_codes": (_c_int, [_vp, _c_i64, _c_i64, _c_int, _vp, _vp]),
+    "msg_unpack_codes": (_c_int, [_vp, _c_i64, _c_i64, _c_int, _vp, _vp]),
+    "msg_group_indices": (_c_int, [_vp, _c_i64, _c_i64, _c_int, _c_int, _vp, _vp]),
+    "msg_encode_values": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_int, _vp, _vp, _vp, _vp]),
+    "msg_lut_build": (_c_int, [_vp, _c_int, _c_i64, _c_i64, _c_int, _vp, _c_int, _c_i64,
+                               _c_i64, _vp, _vp]),
+    "msg_repacked_bytes": (_c_i64, [_c_i64, _c_i64, _c_int, _c_int]),
+    "msg_repack": (_c_int, [_vp, _c_i64, _c_i64, _c_int, _c_int, _c_int, _vp, _vp]),
+    "msg_gemm_plan": (_c_int, [_c_i64, _c_i64, _c_int, _vp, _c_int, _c_i64, _c_int, _c_int,
+                               _c_i64, _c_int, _vp, _vp, _vp]),
+    "msg_gemm": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_int, _vp, _vp, _c_int, _c_i64, _c_int,
+                          _c_int, _c_i64, _vp, _c_int, _vp, _c_int, _vp, _c_i64, _c_int, _vp]),
+    "msg_dequant_mma_workspace_bytes": (_c_i64, [_c_i64, _c_i64, _c_i64]),
+    "msg_dequant_mma": (_c_int, [_vp, _c_i64, _c_i64, _vp, _vp, _c_i64, _vp, _vp, _c_i64,
+                                 _vp]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+class TableBudgetError(MemoryError):
+    """The requested lookup table does not fit in the memory budget (lut.py:30-31)."""
+
+
+def load_library(path: Path | None = None) -> ctypes.CDLL:
+    """Load (once) and type the C-ABI library.  Raises if it is missing."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        p = Path(path) if path else LIB_PATH
+        if not p.exists():
+            raise RuntimeError(
+                f"msgemm_b200 CUDA library not built ({p}); run "
+                "`python -m paper_2310_06178_b200.build` -- there is no CPU fallback")
+        lib = ctypes.CDLL(str(p))
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def lib() -> ctypes.CDLL:
+    return _lib if _lib is not None else load_library()
+
+
+def check(status: int) -> None:
+    if status == MSG_OK:
+        return
+    msg = lib().msg_last_error().decode(errors="replace")
+    if status == MSG_ERR_VALUE or status == MSG_ERR_WORKSPACE:
+        raise ValueError(msg)
+    if status == MSG_ERR_INDEX:
+        raise IndexError(msg)
+    if status == MSG_ERR_BUDGET:
+        raise TableBudgetError(msg)
+    if status == MSG_ERR_UNSUPPORTED:
+        raise NotImplementedError(msg)
+    raise RuntimeError(f"msgemm_b200 CUDA error: {msg}")
+
+
+# --------------------------------------------------------------------------
+# torch / device plumbing
+# --------------------------------------------------------------------------
+
+def torch():
+    import torch as _t
+    return _t
+
+
+def require_device():
+    """The CUDA device this call runs on; raise loudly if there is none."""
+    t = torch()
+    if not t.cuda.is_available():
+        raise RuntimeError("msgemm_b200 needs a CUDA device (B200, sm_100a); "
+                           "there is no CPU fallback")
+    lib()
+    return t.device("cuda", t.cuda.current_device())
+
+
+def stream_ptr():
+    return ctypes.c_void_p(torch().cuda.current_stream().cuda_stream)
+
+
+def ptr(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr() if t is not None else 0)
+
+
+def host_doubles(values) -> ctypes.Array:
+    vals = [float(v) for v in values]
+    return (ctypes.c_double * len(vals))(*vals)
+
+
+_NP2CODE = {
+    np.dtype(np.float32): F32, np.dtype(np.float16): F16, np.dtype(np.float64): F64,
+    np.dtype(np.int32): I32, np.dtype(np.int64): I64, np.dtype(np.uint8): U8,
+    np.dtype(np.int8): I8, np.dtype(np.int16): I16,
+}
+
+
+def dtype_code(dt) -> int:
+    """MSG_* element code of a numpy or torch dtype."""
+    t = torch()
+    if isinstance(dt, t.dtype):
+        m = {t.float32: F32, t.float16: F16, t.float64: F64, t.int32: I32, t.int64: I64,
+             t.uint8: U8, t.int8: I8, t.int16: I16, t.bfloat16: BF16}
+        if dt not in m:
+            raise NotImplementedError(f"dtype {dt} is not supported on the GPU path")
+        return m[dt]
+    nd = np.dtype(dt)
+    if nd not in _NP2CODE:
+        raise NotImplementedError(f"dtype {nd} is not supported on the GPU path")
+    return _NP2CODE[nd]
+
+
+def torch_dtype_of(np_dtype):
+    t = torch()
+    return {np.dtype(np.float32): t.float32, np.dtype(np.float16): t.float16,
+            np.dtype(np.float64): t.float64, np.dtype(np.int32): t.int32,
+            np.dtype(np.int64): t.int64, np.dtype(np.uint8): t.uint8,
+            np.dtype(np.int8): t.int8, np.dtype(np.int16): t.int16}[np.dtype(np_dtype)]
+
+
+def is_torch(x) -> bool:
+    try:
+        return isinstance(x, torch().Tensor)
+    except Exception:  # pragma: no cover
+        return False
+
+
+def to_device(x, dev, non_blocking: bool = False):
+    """Contiguous device tensor view/copy of a numpy array or tensor."""
+    t = torch()
+    if is_torch(x):
+        return x.to(dev, non_blocking=non_blocking).contiguous()
+    a = np.ascontiguousarray(x)
+    return t.from_numpy(a).to(dev, non_blocking=False)
+
+
+_ws = {}
+
+
+def workspace(nbytes: int, dev):
+    """Per-(device, stream) scratch buffer, grown on demand, never freed on the hot path."""
+    t = torch()
+    key = (dev.index, t.cuda.current_stream(dev).cuda_stream)
+    buf = _ws.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = t.empty(max(int(nbytes), 256), dtype=t.uint8, device=dev)
+        _ws[key] = buf
+    return buf

@@ -1,0 +1,137 @@
+// Shared helpers for the msGeMM sm_100a kernels: error plumbing, element
+// types, codebook parameter block.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+
+#include "msgemm_b200.h"
+
+namespace msg {
+
+// ----------------------------------------------------------------------------
+// errors (thread-local message, negative status codes)
+// ----------------------------------------------------------------------------
+void set_error(const std::string& s);
+int fail(int code, const char* fmt, ...);
+
+#define MSG_CUDA_CHECK(expr)                                                   \
+  do {                                                                         \
+    cudaError_t err__ = (expr);                                                \
+    if (err__ != cudaSuccess)                                                  \
+      return ::msg::fail(MSG_ERR_CUDA, "%s failed: %s", #expr,                 \
+                         cudaGetErrorString(err__));                           \
+  } while (0)
+
+#define MSG_LAUNCH_CHECK() MSG_CUDA_CHECK(cudaGetLastError())
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int sm_count();  // cached multiProcessorCount of the current device
+int max_smem_optin();
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+inline int row_bytes(int64_t k, int width) {
+  // packing.py:39-47 bytes_per_row
+  if (width == 4) return (int)((k + 1) / 2);
+  if (width == 2) return (int)((k + 3) / 4);
+  return (int)k;
+}
+
+// ----------------------------------------------------------------------------
+// codebook parameter block: up to 256 values (width <= 8), passed by value
+// ----------------------------------------------------------------------------
+struct CodebookParam {
+  double v[256];
+  int width;
+  int n;
+};
+
+inline CodebookParam make_codebook(const double* values, int width) {
+  CodebookParam cb{};
+  cb.width = width;
+  cb.n = 1 << width;
+  for (int i = 0; i < cb.n; ++i) cb.v[i] = values[i];
+  return cb;
+}
+
+// ----------------------------------------------------------------------------
+// element type traits
+// ----------------------------------------------------------------------------
+inline int dtype_size(int dt) {
+  switch (dt) {
+    case MSG_F32: case MSG_I32: return 4;
+    case MSG_F16: case MSG_I16: case MSG_BF16: return 2;
+    case MSG_F64: case MSG_I64: return 8;
+    case MSG_U8: case MSG_I8: return 1;
+  }
+  return 0;
+}
+inline bool dtype_is_int(int dt) {
+  return dt == MSG_I32 || dt == MSG_I64 || dt == MSG_U8 || dt == MSG_I8 || dt == MSG_I16;
+}
+
+// load element i of a typed array as T
+template <typename T>
+__device__ __forceinline__ T load_as(const void* p, int dt, int64_t i);
+
+template <>
+__device__ __forceinline__ double load_as<double>(const void* p, int dt, int64_t i) {
+  switch (dt) {
+    case MSG_F32: return (double)((const float*)p)[i];
+    case MSG_F16: return (double)__half2float(((const __half*)p)[i]);
+    case MSG_F64: return ((const double*)p)[i];
+    case MSG_I32: return (double)((const int32_t*)p)[i];
+    case MSG_I64: return (double)((const int64_t*)p)[i];
+    case MSG_U8: return (double)((const uint8_t*)p)[i];
+    case MSG_I8: return (double)((const int8_t*)p)[i];
+    case MSG_I16: return (double)((const int16_t*)p)[i];
+  }
+  return 0.0;
+}
+
+template <>
+__device__ __forceinline__ int64_t load_as<int64_t>(const void* p, int dt, int64_t i) {
+  switch (dt) {
+    case MSG_I32: return (int64_t)((const int32_t*)p)[i];
+    case MSG_I64: return ((const int64_t*)p)[i];
+    case MSG_U8: return (int64_t)((const uint8_t*)p)[i];
+    case MSG_I8: return (int64_t)((const int8_t*)p)[i];
+    case MSG_I16: return (int64_t)((const int16_t*)p)[i];
+    case MSG_F32: return (int64_t)((const float*)p)[i];
+    case MSG_F64: return (int64_t)((const double*)p)[i];
+    case MSG_F16: return (int64_t)__half2float(((const __half*)p)[i]);
+  }
+  return 0;
+}
+
+template <>
+__device__ __forceinline__ float load_as<float>(const void* p, int dt, int64_t i) {
+  switch (dt) {
+    case MSG_F32: return ((const float*)p)[i];
+    case MSG_F16: return __half2float(((const __half*)p)[i]);
+    default: return (float)load_as<double>(p, dt, i);
+  }
+}
+
+// store a value held in accumulator type A into a typed array
+template <typename A>
+__device__ __forceinline__ void store_as(void* p, int dt, int64_t i, A v) {
+  switch (dt) {
+    case MSG_F32: ((float*)p)[i] = (float)v; break;
+    case MSG_F16: ((__half*)p)[i] = __float2half_rn((float)v); break;
+    case MSG_F64: ((double*)p)[i] = (double)v; break;
+    case MSG_I32: ((int32_t*)p)[i] = (int32_t)(int64_t)v; break;
+    case MSG_I64: ((int64_t*)p)[i] = (int64_t)v; break;
+    case MSG_I16: ((int16_t*)p)[i] = (int16_t)(int64_t)v; break;
+    case MSG_I8: ((int8_t*)p)[i] = (int8_t)(int64_t)v; break;
+    case MSG_U8: ((uint8_t*)p)[i] = (uint8_t)(int64_t)v; break;
+  }
+}
+
+}  // namespace msg

@@ -1,0 +1,224 @@
+// Weight-format kernels: nibble pack/unpack, value encoding, group indices.
+//
+// Device restatements of the reference's packing module
+// (/root/reference/pkg/src/msgemm/packing.py).  Layout contract
+// (packing.py:99-128): width 4 -> column j in byte j/2, even j in the low
+// nibble; width 2 -> column j in byte j/4 at bit 2*(j%4); other widths -> one
+// code per byte.  Group index (packing.py:201-228): first code least
+// significant, idx = sum_r code(j*d + r) << (width*r).
+#include <cstdarg>
+#include <mutex>
+
+#include "msg_common.cuh"
+
+namespace msg {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& s) { g_last_error = s; }
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+int sm_count() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cached[dev]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = n > 0 ? n : 148;
+  }
+  return cached[dev];
+}
+
+int max_smem_optin() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cached[dev]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cached[dev] = n > 0 ? n : 227 * 1024;
+  }
+  return cached[dev];
+}
+
+// code of column j in a packed row
+__device__ __forceinline__ uint32_t code_at(const uint8_t* row, int64_t j, int width) {
+  if (width == 4) return (row[j >> 1] >> ((j & 1) * 4)) & 0xF;
+  if (width == 2) return (row[j >> 2] >> ((j & 3) * 2)) & 0x3;
+  return row[j];
+}
+
+// ---------------------------------------------------------------- pack codes
+__global__ void pack_codes_kernel(const uint8_t* __restrict__ codes, int64_t m, int64_t k,
+                                  int width, int rb, uint8_t* __restrict__ out) {
+  int64_t n = m * (int64_t)rb;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = t / rb, byte = t - i * rb;
+    const uint8_t* row = codes + i * k;
+    uint32_t v = 0;
+    if (width == 4 || width == 2) {
+      int per = 8 / width;
+      for (int s = 0; s < per; ++s) {
+        int64_t j = byte * per + s;
+        if (j < k) v |= (uint32_t)(row[j] & ((1u << width) - 1)) << (width * s);
+      }
+    } else {
+      v = row[byte];
+    }
+    out[t] = (uint8_t)v;
+  }
+}
+
+// -------------------------------------------------------------- unpack codes
+__global__ void unpack_codes_kernel(const uint8_t* __restrict__ packed, int64_t m, int64_t k,
+                                    int width, int rb, uint8_t* __restrict__ codes) {
+  int64_t n = m * k;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = t / k, j = t - i * k;
+    codes[t] = (uint8_t)code_at(packed + i * rb, j, width);
+  }
+}
+
+// ------------------------------------------------------------ group indices
+__global__ void group_indices_kernel(const uint8_t* __restrict__ packed, int64_t m, int64_t k,
+                                     int width, int d, int rb, int64_t* __restrict__ out) {
+  int64_t nb = k / d;
+  int64_t n = m * nb;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = t / nb, j = t - i * nb;
+    const uint8_t* row = packed + i * rb;
+    int64_t idx = 0;
+    for (int r = 0; r < d; ++r) idx |= (int64_t)code_at(row, j * d + r, width) << (width * r);
+    out[t] = idx;
+  }
+}
+
+// ------------------------------------------------------------ value encoding
+// nearest codebook value, |w - v| <= 1e-6 |v| or both zero (packing.py:146-169)
+__global__ void encode_values_kernel(const double* __restrict__ w, const double* __restrict__ grid,
+                                     int64_t m, int64_t k, int width, CodebookParam cb, int rb,
+                                     uint8_t* __restrict__ out,
+                                     unsigned long long* __restrict__ bad) {
+  int64_t n = m * (int64_t)rb;
+  int per = (width == 4 || width == 2) ? 8 / width : 1;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = t / rb, byte = t - i * rb;
+    uint32_t packedv = 0;
+    for (int s = 0; s < per; ++s) {
+      int64_t j = byte * per + s;
+      if (j >= k) break;
+      int64_t e = i * k + j;
+      double x = w[e];
+      if (grid) x = x / grid[e];
+      int best = 0;
+      double bd = fabs(x - cb.v[0]);
+      for (int c = 1; c < cb.n; ++c) {
+        double dd = fabs(x - cb.v[c]);
+        if (dd < bd) { bd = dd; best = c; }
+      }
+      double got = cb.v[best];
+      bool ok = (fabs(x - got) <= 1e-6 * fabs(got)) || (x == 0.0 && got == 0.0);
+      if (!ok) {
+        atomicAdd(&bad[0], 1ull);
+        atomicMin(&bad[1], (unsigned long long)e);
+      }
+      packedv |= (uint32_t)best << (per > 1 ? width * s : 0);
+    }
+    out[t] = (uint8_t)packedv;
+  }
+}
+
+static int grid_for(int64_t n) {
+  int64_t g = ceil_div(n, 256);
+  int64_t cap = (int64_t)sm_count() * 16;
+  return (int)(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+static int check_width(int width) {
+  if (width < 2 || width > 8) return fail(MSG_ERR_VALUE, "width must be in 2..8, got %d", width);
+  return MSG_OK;
+}
+
+}  // namespace msg
+
+using namespace msg;
+
+extern "C" {
+
+const char* msg_last_error(void) { return g_last_error.c_str(); }
+
+int msg_version(void) { return 100; }
+
+int msg_device_sm_count(void) { return sm_count(); }
+
+int msg_pack_codes(const uint8_t* codes, int64_t m, int64_t k, int width, uint8_t* packed,
+                   void* stream) {
+  if (int e = check_width(width)) return e;
+  if (m < 0 || k < 0) return fail(MSG_ERR_VALUE, "matrix dimensions must be non-negative");
+  int rb = row_bytes(k, width);
+  int64_t n = m * rb;
+  if (n == 0) return MSG_OK;
+  pack_codes_kernel<<<grid_for(n), 256, 0, as_stream(stream)>>>(codes, m, k, width, rb, packed);
+  MSG_LAUNCH_CHECK();
+  return MSG_OK;
+}
+
+int msg_unpack_codes(const uint8_t* packed, int64_t m, int64_t k, int width, uint8_t* codes,
+                     void* stream) {
+  if (int e = check_width(width)) return e;
+  int rb = row_bytes(k, width);
+  int64_t n = m * k;
+  if (n == 0) return MSG_OK;
+  unpack_codes_kernel<<<grid_for(n), 256, 0, as_stream(stream)>>>(packed, m, k, width, rb, codes);
+  MSG_LAUNCH_CHECK();
+  return MSG_OK;
+}
+
+int msg_group_indices(const uint8_t* packed, int64_t m, int64_t k, int width, int d,
+                      int64_t* out, void* stream) {
+  if (d < 1) return fail(MSG_ERR_VALUE, "depth d must be >= 1");
+  if (d * width > 32)
+    return fail(MSG_ERR_VALUE, "d*width = %d exceeds 32-bit index limit", d * width);
+  int rb = row_bytes(k, width);
+  int64_t n = m * (k / d);
+  if (n == 0) return MSG_OK;
+  group_indices_kernel<<<grid_for(n), 256, 0, as_stream(stream)>>>(packed, m, k, width, d, rb,
+                                                                    out);
+  MSG_LAUNCH_CHECK();
+  return MSG_OK;
+}
+
+int msg_encode_values(const double* weights, const double* grid, int64_t m, int64_t k, int width,
+                      const double* values, uint8_t* packed, int64_t* bad, void* stream) {
+  if (int e = check_width(width)) return e;
+  int rb = row_bytes(k, width);
+  int64_t n = m * rb;
+  cudaStream_t s = as_stream(stream);
+  // bad[0] = count, bad[1] = first flat index (UINT64_MAX when none)
+  unsigned long long init[2] = {0ull, ~0ull};
+  MSG_CUDA_CHECK(cudaMemcpyAsync(bad, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  if (n == 0) return MSG_OK;
+  CodebookParam cb = make_codebook(values, width);
+  encode_values_kernel<<<grid_for(n), 256, 0, s>>>(weights, grid, m, k, width, cb, rb, packed,
+                                                   reinterpret_cast<unsigned long long*>(bad));
+  MSG_LAUNCH_CHECK();
+  return MSG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,256 @@
+"""Phase 2: msGeMM on the GPU (mirror of reference gemm.py:24-231).
+
+``msgemm`` keeps the reference's signature, validation order, output
+dtype/shape and error types (gemm.py:89-153) and runs the CUDA path:
+
+* widths 4, float16/float32 activations, d <= 3, no per-group scales: the
+  fused kernel (K3 repack once per weight, then one launch that builds the
+  tables in shared memory and gathers, plus a deterministic reduction);
+* everything else the reference accepts (d up to 7, widths 2..8, int/f64
+  activations, per-group scales): the generic global-memory-table kernels.
+
+Numpy inputs give numpy outputs (the drop-in contract); CUDA tensors give
+CUDA tensors with no host round trip.  There is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import TableBudgetError
+from .lut import DEFAULT_BUDGET, block_nbytes, build_lut
+from .packing import PackedWeightMatrix, PerGroup, PerRow, group_indices
+
+__all__ = ["OpCount", "msgemm", "msgemm_counted", "msgemm_traced", "naive_gemm",
+           "naive_gemm_counted"]
+
+
+@dataclass(frozen=True)
+class OpCount:
+    """Arithmetic / memory-access counts for one execution (gemm.py:24-47)."""
+
+    fma: int = 0
+    add: int = 0
+    mul: int = 0
+    mem_weights: int = 0
+    mem_activations: int = 0
+
+    def __add__(self, other: "OpCount") -> "OpCount":
+        return OpCount(self.fma + other.fma, self.add + other.add, self.mul + other.mul,
+                       self.mem_weights + other.mem_weights,
+                       self.mem_activations + other.mem_activations)
+
+
+def _as_matrix(X):
+    """(k, b) view of X and whether X was a vector (gemm.py:50-57)."""
+    if _lib.is_torch(X):
+        if X.dim() == 1:
+            return X[:, None], True
+        if X.dim() != 2:
+            raise ValueError("activations must be a vector or a (k, b) matrix")
+        return X, False
+    X = np.asarray(X)
+    if X.ndim == 1:
+        return X[:, None], True
+    if X.ndim != 2:
+        raise ValueError("activations must be a vector or a (k, b) matrix")
+    return X, False
+
+
+def _check_scales_for_depth(pwm, d: int) -> None:
+    """gemm.py:60-67."""
+    if isinstance(pwm.scales, PerGroup):
+        r = pwm.scales.group_size
+        if r < d or r % d != 0:
+            raise ValueError(f"per-group scaling needs group_size >= d and divisible by d; "
+                             f"got group_size={r}, d={d}")
+
+
+def _np_dtype(X):
+    if _lib.is_torch(X):
+        t = _lib.torch()
+        return {t.float32: np.float32, t.float16: np.float16, t.float64: np.float64,
+                t.int32: np.int32, t.int64: np.int64, t.uint8: np.uint8, t.int8: np.int8,
+                t.int16: np.int16}.get(X.dtype, None)
+    return X.dtype
+
+
+def _ensure_device_pwm(pwm):
+    """Accept our PackedWeightMatrix or any duck-typed equivalent (e.g. the reference's)."""
+    if isinstance(pwm, PackedWeightMatrix):
+        return pwm
+    return PackedWeightMatrix(m=pwm.m, k=pwm.k, width=pwm.width, data=pwm.data,
+                              codebook=pwm.codebook, scales=pwm.scales)
+
+
+def msgemm(pwm: PackedWeightMatrix, X, d: int, budget: int = DEFAULT_BUDGET,
+           workers: int = 1, *, table_dtype=None, symmetric: bool = True,
+           out_dtype=None, out=None, _flags: int = 0):
+    """Two-phase GeMM Y = W @ X on the GPU (gemm.py:89-153).
+
+    Returns (m, b), or (m,) for a vector X, in X's dtype.  ``budget`` keeps
+    the reference's TableBudgetError contract (a single table block larger
+    than the budget); ``workers`` is accepted and ignored (results never
+    depend on it).  Keyword-only extensions:
+
+    table_dtype: None (tables in X's dtype, as the reference) or
+        "float32" (fp32 tables for fp16 X -- exact for integer-valued X).
+    symmetric: use sign-symmetric half tables when the codebook allows.
+    out_dtype: None (Y in X's dtype, as the reference) or a float dtype,
+        e.g. float32 Y from fp16 X (the bit-exact integer check).
+    out: optional preallocated CUDA tensor for Y (torch inputs only).
+    """
+    pwm = _ensure_device_pwm(pwm)
+    Xm, was_vector = _as_matrix(X)
+    if int(Xm.shape[0]) != pwm.k:
+        raise ValueError(f"activation rows {Xm.shape[0]} != weight columns {pwm.k}")
+    if d < 1:
+        raise ValueError("depth d must be >= 1")
+    _check_scales_for_depth(pwm, d)
+    if d * pwm.width > 32:  # group_indices check, gemm.py:107 -> packing.py:221-224
+        raise ValueError(f"d*width = {d * pwm.width} exceeds 32-bit index limit")
+    npdt = _np_dtype(Xm)
+    itemsize = Xm.element_size() if _lib.is_torch(Xm) else Xm.dtype.itemsize
+    if 2 ** (pwm.width * d) * itemsize > budget:
+        raise TableBudgetError("a single table block exceeds the memory budget")
+
+    dev = _lib.require_device()
+    t = _lib.torch()
+    lib = _lib.lib()
+    m, k, b = pwm.m, pwm.k, int(Xm.shape[1])
+    x_code = _lib.dtype_code(Xm.dtype)
+    is_tensor = _lib.is_torch(X)
+    on_device = is_tensor and X.is_cuda
+
+    scale_mode, group_size, q_code = _lib.SCALE_NONE, 0, _lib.F64
+    if isinstance(pwm.scales, PerRow):
+        scale_mode = _lib.SCALE_PER_ROW
+    elif isinstance(pwm.scales, PerGroup):
+        scale_mode, group_size = _lib.SCALE_PER_GROUP, pwm.scales.group_size
+    qd = pwm.device_scales(dev)
+    if qd is not None:
+        q_code = _lib.dtype_code(qd.dtype)
+        if q_code == _lib.BF16:
+            raise NotImplementedError("bfloat16 scales are not supported")
+
+    flags = int(_flags)
+    if table_dtype is not None and np.dtype(table_dtype) == np.float32:
+        flags |= _lib.FLAG_F32_ENTRIES
+    if not symmetric:
+        flags |= _lib.FLAG_NO_SYMMETRY
+
+    vals = _lib.host_doubles(pwm.codebook.values)
+    layout, sym = _lib.ctypes.c_int(0), _lib.ctypes.c_int(0)
+    ws_bytes = _lib.ctypes.c_int64(0)
+    _lib.check(lib.msg_gemm_plan(m, k, pwm.width, vals, x_code, b, d, scale_mode, group_size,
+                                 flags, _lib.ctypes.byref(layout), _lib.ctypes.byref(sym),
+                                 _lib.ctypes.byref(ws_bytes)))
+    xd = _lib.to_device(Xm, dev, non_blocking=is_tensor and not on_device and Xm.is_pinned())
+    y_dt = xd.dtype if out_dtype is None else _lib.torch_dtype_of(np.dtype(out_dtype))
+    host_out = None
+    if out is not None:
+        if tuple(out.shape) not in ((m, b), (m,)) or out.dtype != y_dt or not out.is_contiguous():
+            raise ValueError("out must be a contiguous tensor of shape (m, b) and Y's dtype")
+        if out.is_cuda:
+            Y = out
+        else:
+            host_out = out
+            Y = t.empty((m, b), dtype=y_dt, device=dev)
+    else:
+        Y = t.empty((m, b), dtype=y_dt, device=dev)
+    y_code = _lib.dtype_code(y_dt)
+    if m and b:
+        wrep = (pwm.device_layout(dev, d, layout.value, sym.value)
+                if layout.value != _lib.LAYOUT_NONE else None)
+        ws = _lib.workspace(ws_bytes.value, dev)
+        _lib.check(lib.msg_gemm(
+            _lib.ptr(pwm.device_data(dev)), _lib.ptr(wrep), m, k, pwm.width, vals,
+            _lib.ptr(xd), x_code, b, d, scale_mode, group_size, _lib.ptr(qd), q_code,
+            _lib.ptr(Y), y_code, _lib.ptr(ws), ws.numel(), flags, _lib.stream_ptr()))
+    if host_out is not None:          # host tensor out (e.g. pinned): one D2H, synchronous
+        host_out.copy_(Y.reshape(host_out.shape))
+        return host_out
+    if was_vector:
+        Y = Y.reshape(m, b)[:, 0]
+    if on_device:
+        return Y
+    if is_tensor:
+        return Y.cpu()
+    return Y.cpu().numpy()
+
+
+def msgemm_counted(pwm: PackedWeightMatrix, X, d: int, budget: int = DEFAULT_BUDGET,
+                   workers: int = 1):
+    """msgemm plus shape-derived operation counts (gemm.py:156-183)."""
+    Xm, _ = _as_matrix(X)
+    if pwm.k % d != 0:
+        raise ValueError("op counting requires k divisible by d")
+    Y = msgemm(pwm, X, d, budget=budget, workers=workers)
+    b = int(Xm.shape[1])
+    nb = pwm.k // d
+    mul = 0
+    if isinstance(pwm.scales, PerRow):
+        mul = pwm.m * b
+    elif isinstance(pwm.scales, PerGroup):
+        mul = pwm.m * (pwm.k // pwm.scales.group_size) * b
+    return Y, OpCount(fma=2 ** (pwm.codebook.width * d) * d * nb * b,
+                      add=(nb - 1) * pwm.m * b, mul=mul,
+                      mem_weights=pwm.m * pwm.k * b, mem_activations=pwm.k * b)
+
+
+def msgemm_traced(pwm: PackedWeightMatrix, x, d: int, budget: int = DEFAULT_BUDGET):
+    """Matrix-vector msgemm with the lookup trace (gemm.py:186-203)."""
+    if (x.dim() if _lib.is_torch(x) else np.asarray(x).ndim) != 1:
+        raise ValueError("tracing is defined for a single activation vector")
+    y = msgemm(pwm, x, d, budget=budget)
+    idx = group_indices(pwm, d)
+    table = build_lut(x, pwm.codebook, d, budget=budget)
+    idx_h = idx.cpu().numpy() if _lib.is_torch(idx) else idx
+    ent = table.entries.cpu().numpy() if _lib.is_torch(table.entries) else table.entries
+    trace = [[(j, int(idx_h[i, j]), ent[j, idx_h[i, j]]) for j in range(idx_h.shape[1])]
+             for i in range(pwm.m)]
+    return y, trace
+
+
+def naive_gemm(W, X):
+    """Dense reference W @ X (gemm.py:206-216), on the GPU (cuBLAS via torch).
+
+    Integer inputs are accumulated exactly: in float64 when every partial sum
+    provably stays below 2^53, else the call refuses (NotImplementedError)
+    rather than round.
+    """
+    t = _lib.torch()
+    on_device = _lib.is_torch(X) or _lib.is_torch(W)
+    Wa = W if _lib.is_torch(W) else np.asarray(W)
+    Xm, was_vector = _as_matrix(X)
+    if Wa.ndim != 2 or Wa.shape[1] != Xm.shape[0]:
+        raise ValueError(f"shape mismatch: W {tuple(Wa.shape)} x X {tuple(Xm.shape)}")
+    dev = _lib.require_device()
+    wd, xd = _lib.to_device(Wa, dev), _lib.to_device(Xm, dev)
+    ints = not wd.is_floating_point() and not xd.is_floating_point()
+    if ints:
+        bound = (float(wd.abs().max()) if wd.numel() else 0.0) * \
+                (float(xd.abs().max()) if xd.numel() else 0.0) * max(int(wd.shape[1]), 1)
+        if bound >= 2.0 ** 53:
+            raise NotImplementedError("integer naive_gemm beyond exact float64 range")
+        Y = (wd.double() @ xd.double()).round().to(t.int64)
+    else:
+        res = np.result_type(_np_dtype(wd) or np.float64, _np_dtype(xd) or np.float64)
+        ct = _lib.torch_dtype_of(res)
+        Y = wd.to(ct) @ xd.to(ct)
+    if was_vector:
+        Y = Y[:, 0]
+    return Y if on_device else Y.cpu().numpy()
+
+
+def naive_gemm_counted(W, X):
+    """naive_gemm plus the m*k*b FMA count (gemm.py:219-231)."""
+    Wa = W if _lib.is_torch(W) else np.asarray(W)
+    Xm, _ = _as_matrix(X)
+    Y = naive_gemm(W, X)
+    m, k = (int(s) for s in Wa.shape)
+    b = int(Xm.shape[1])
+    return Y, OpCount(fma=m * k * b, mem_weights=m * k, mem_activations=k * b)
