@@ -4,24 +4,28 @@
 // reduction, k%d tail, per-row scale), lut.py:59-72 (table entries),
 // packing.py:201-228 (group index: first code least significant).
 //
-// Design (sm_100a, one CTA per SM):
+// Design (sm_100a, one 256-thread CTA per SM):
 //   * K3 repacks the reference's row-major nibbles (packing.py:99-114) into
 //     "quad planes": for every 4 consecutive d-groups and every row, a 32-bit
 //     word of low index bytes (d=2,3; 16 bits for d=1) and, for d=3, a 16-bit
-//     word of high index nibbles.  Density stays 4*d bits per group, and a
-//     warp reading one plane word for 32 consecutive rows issues one
-//     coalesced 128-byte request.  For antisymmetric codebooks
-//     (v[c] + v[~c] = 2*beta, e.g. two's-complement int4 with beta = -1/2)
-//     K3 folds the sign symmetry into the stored index: an index with the top
-//     bit set is stored complemented with a sign bit, so tables hold only
-//     2^(4d-1) entries: L(idx) = +-H[f] + beta*(x_0 + .. + x_{d-1}).
+//     word of high index nibbles.  Density stays 4*d bits per group.  Plane
+//     rows are padded to a multiple of 8 so a row block of a quad is one
+//     16-byte-aligned contiguous span -> one TMA bulk copy.  For
+//     antisymmetric codebooks (v[c] + v[~c] = 2*beta, e.g. two's-complement
+//     int4 with beta = -1/2) K3 folds the sign symmetry into the stored index:
+//     an index with the top bit set is stored complemented, plus a sign bit,
+//     so tables hold only 2^(4d-1) entries and
+//         L(idx) = +-H[f] + beta * (x_0 + .. + x_{d-1}).
 //   * The fused kernel gives each CTA a block of R = 256*RPT rows, a k-slice
 //     of quads and a tile of BC batch columns.  Per round it builds the
 //     tables of QL quads (4*QL groups x ES entries x BC columns, batch
 //     innermost so one vector LDS fetches all BC columns of an entry) into
-//     shared memory, then every thread gathers for its RPT rows and
-//     accumulates fp32 in registers.  Tables are built once per (row block,
-//     k-slice); the build is amortised over R rows.
+//     shared memory and every thread gathers for its RPT rows, accumulating
+//     fp32 in registers with packed FFMA2.  The weight words of round t+1 are
+//     brought in by cp.async.bulk (TMA bulk copy) into a double-buffered
+//     staging area while round t builds and gathers; the activations of round
+//     t+1 are prefetched into registers.  Tables are built once per (row
+//     block, k-slice) and amortised over R rows.
 //   * k-slice partials go to a workspace [S][m][b] (fp32) and a second,
 //     deterministic pass sums them in slice order, adds the k%d tail, the
 //     symmetry correction and the per-row scale, and casts to Y's dtype.
@@ -44,7 +48,7 @@ static inline int64_t align256(int64_t v) { return (v + 255) / 256 * 256; }
 // K3: quad-plane repack
 // ============================================================================
 struct QuadLayout {
-  int64_t nb, nq, tail;
+  int64_t nb, nq, tail, mp;  // mp: plane row stride (m rounded up to 8)
   int64_t lo_off, hi_off, tail_off, total;
   int lo_bytes;  // 4 for d=2,3 ; 2 for d=1
   bool has_hi;
@@ -55,11 +59,12 @@ static QuadLayout quad_layout(int64_t m, int64_t k, int d) {
   L.nb = k / d;
   L.nq = (L.nb + 3) / 4;
   L.tail = k - L.nb * d;
+  L.mp = (m + 7) / 8 * 8;
   L.lo_bytes = d == 1 ? 2 : 4;
   L.has_hi = d == 3;
   L.lo_off = 0;
-  L.hi_off = align256(L.nq * m * L.lo_bytes);
-  L.tail_off = L.hi_off + (L.has_hi ? align256(L.nq * m * 2) : 0);
+  L.hi_off = align256(L.nq * L.mp * L.lo_bytes);
+  L.tail_off = L.hi_off + (L.has_hi ? align256(L.nq * L.mp * 2) : 0);
   L.total = L.tail_off + (L.tail ? align256(m * 2) : 0);
   if (L.total == 0) L.total = 256;
   return L;
@@ -69,41 +74,103 @@ __device__ __forceinline__ uint32_t nib(const uint8_t* row, int64_t j) {
   return (row[j >> 1] >> ((j & 1) * 4)) & 0xF;
 }
 
-// one thread per (quad, row): rows fastest so plane stores coalesce
+// one thread per (quad, padded row): rows fastest so plane stores coalesce
 __global__ void repack_quad_kernel(const uint8_t* __restrict__ packed, int64_t m, int64_t k,
                                    int d, int rb, int symmetric, QuadLayout L,
                                    uint8_t* __restrict__ out) {
-  const int64_t total = L.nq * m;
+  const int64_t total = L.nq * L.mp;
   const int bits = 4 * d;
   const uint32_t emask = (1u << bits) - 1;
   const uint32_t top = 1u << (bits - 1);
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t q = t / m, i = t - q * m;
-    const uint8_t* row = packed + i * rb;
+    int64_t q = t / L.mp, i = t - q * L.mp;
     uint32_t lo = 0, hi = 0;
-    for (int g = 0; g < 4; ++g) {
-      int64_t j = q * 4 + g;
-      uint32_t st = 0;
-      if (j < L.nb) {
-        uint32_t idx = 0;
-        for (int r = 0; r < d; ++r) idx |= nib(row, j * d + r) << (4 * r);
-        if (symmetric && (idx & top)) idx = (idx ^ emask) | top;  // complement, keep sign bit
-        st = idx;
+    if (i < m) {
+      const uint8_t* row = packed + i * rb;
+      for (int g = 0; g < 4; ++g) {
+        // position g of row i holds group (g + i) % 4 of the quad: the lanes of a
+        // warp (consecutive rows) then hit 4 different tables at every step
+        int64_t j = q * 4 + ((g + i) & 3);
+        uint32_t st = 0;
+        if (j < L.nb) {
+          uint32_t idx = 0;
+          for (int r = 0; r < d; ++r) idx |= nib(row, j * d + r) << (4 * r);
+          if (symmetric && (idx & top)) idx = (idx ^ emask) | top;  // complement + sign bit
+          st = idx;
+        }
+        if (d == 1) lo |= st << (4 * g);
+        else if (d == 2) lo |= st << (8 * g);
+        else { lo |= (st & 0xFF) << (8 * g); hi |= (st >> 8) << (4 * g); }
       }
-      if (d == 1) lo |= st << (4 * g);
-      else if (d == 2) lo |= st << (8 * g);
-      else { lo |= (st & 0xFF) << (8 * g); hi |= (st >> 8) << (4 * g); }
+      if (L.tail && q == 0) {
+        uint32_t tc = 0;
+        for (int64_t j = L.nb * d; j < k; ++j) tc |= nib(row, j) << (4 * (j - L.nb * d));
+        reinterpret_cast<uint16_t*>(out + L.tail_off)[i] = (uint16_t)tc;
+      }
     }
     if (d == 1) reinterpret_cast<uint16_t*>(out + L.lo_off)[t] = (uint16_t)lo;
     else reinterpret_cast<uint32_t*>(out + L.lo_off)[t] = lo;
     if (L.has_hi) reinterpret_cast<uint16_t*>(out + L.hi_off)[t] = (uint16_t)hi;
-    if (L.tail && q == 0) {
-      uint32_t tc = 0;
-      for (int64_t j = L.nb * d; j < k; ++j) tc |= nib(row, j) << (4 * (j - L.nb * d));
-      reinterpret_cast<uint16_t*>(out + L.tail_off)[i] = (uint16_t)tc;
-    }
   }
+}
+
+// ============================================================================
+// async-copy and packed-math helpers (PTX)
+// ============================================================================
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// a0,a1 += x0*s, x1*s  (one FFMA2)
+__device__ __forceinline__ void ffma2(float& a0, float& a1, float x0, float x1, float s) {
+  unsigned long long acc, xv, sv;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(acc) : "f"(a0), "f"(a1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(xv) : "f"(x0), "f"(x1));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(sv) : "f"(s));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(xv), "l"(sv));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(acc));
+}
+// e0,e1 = s*x0 + b0, s*x1 + b1
+__device__ __forceinline__ void fma2_to(float& e0, float& e1, float s, float x0, float x1,
+                                        float b0, float b1) {
+  unsigned long long acc, xv, sv;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(acc) : "f"(b0), "f"(b1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(xv) : "f"(x0), "f"(x1));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(sv) : "f"(s));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(xv), "l"(sv));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(e0), "=f"(e1) : "l"(acc));
 }
 
 // ============================================================================
@@ -113,11 +180,10 @@ constexpr int kThreads = 256;
 
 struct FusedParams {
   const uint8_t* wrep;
-  int64_t lo_off, hi_off;
+  int64_t lo_off, hi_off, mp;
   int64_t m, nb, nq;
   const void* x;  // (k, b) row-major, F16 or F32
   int64_t b;
-  int d;
   float s[16];  // per-code value used in tables: v[c] - beta (symmetric) or v[c]
   float beta;
   int quads_per_slice;  // k-slice length in quads
@@ -128,49 +194,106 @@ struct FusedParams {
 
 template <typename XT> __device__ __forceinline__ float ldx(const void* p, int64_t i);
 template <> __device__ __forceinline__ float ldx<float>(const void* p, int64_t i) {
-  return reinterpret_cast<const float*>(p)[i];
+  return __ldg(reinterpret_cast<const float*>(p) + i);
 }
 template <> __device__ __forceinline__ float ldx<__half>(const void* p, int64_t i) {
   return __half2float(reinterpret_cast<const __half*>(p)[i]);
 }
 
-// BC entries of type ET as raw 32-bit words
-template <typename ET, int BC> struct EntryVec {
-  static constexpr int kBytes = BC * (int)sizeof(ET);
-  static constexpr int kWords = kBytes >= 4 ? kBytes / 4 : 1;
-};
+__device__ __forceinline__ float h2f_lo(uint32_t w) {
+  return __half2float(__ushort_as_half((unsigned short)(w & 0xFFFF)));
+}
+__device__ __forceinline__ float h2f_hi(uint32_t w) {
+  return __half2float(__ushort_as_half((unsigned short)(w >> 16)));
+}
 
+// acc[0..BC) += sg * entry (BC values of type ET at p)
 template <typename ET, int BC>
-__device__ __forceinline__ void load_entry(const uint8_t* p, uint32_t (&w)[EntryVec<ET, BC>::kWords]) {
-  constexpr int B = EntryVec<ET, BC>::kBytes;
-  if constexpr (B == 2) {
-    w[0] = *reinterpret_cast<const uint16_t*>(p);
-  } else if constexpr (B == 4) {
-    w[0] = *reinterpret_cast<const uint32_t*>(p);
-  } else if constexpr (B == 8) {
-    uint2 v = *reinterpret_cast<const uint2*>(p);
-    w[0] = v.x; w[1] = v.y;
+__device__ __forceinline__ void gather_acc(const uint8_t* p, float sg, float* acc) {
+  if constexpr (sizeof(ET) == 2) {
+    if constexpr (BC == 1) {
+      acc[0] = fmaf(sg, __half2float(*reinterpret_cast<const __half*>(p)), acc[0]);
+    } else if constexpr (BC == 2) {
+      uint32_t w = *reinterpret_cast<const uint32_t*>(p);
+      ffma2(acc[0], acc[1], h2f_lo(w), h2f_hi(w), sg);
+    } else if constexpr (BC == 4) {
+      uint2 v = *reinterpret_cast<const uint2*>(p);
+      ffma2(acc[0], acc[1], h2f_lo(v.x), h2f_hi(v.x), sg);
+      ffma2(acc[2], acc[3], h2f_lo(v.y), h2f_hi(v.y), sg);
+    } else {
+      uint4 v = *reinterpret_cast<const uint4*>(p);
+      ffma2(acc[0], acc[1], h2f_lo(v.x), h2f_hi(v.x), sg);
+      ffma2(acc[2], acc[3], h2f_lo(v.y), h2f_hi(v.y), sg);
+      ffma2(acc[4], acc[5], h2f_lo(v.z), h2f_hi(v.z), sg);
+      ffma2(acc[6], acc[7], h2f_lo(v.w), h2f_hi(v.w), sg);
+    }
   } else {
+    if constexpr (BC == 1) {
+      acc[0] = fmaf(sg, *reinterpret_cast<const float*>(p), acc[0]);
+    } else if constexpr (BC == 2) {
+      float2 v = *reinterpret_cast<const float2*>(p);
+      ffma2(acc[0], acc[1], v.x, v.y, sg);
+    } else {
 #pragma unroll
-    for (int i = 0; i < B / 16; ++i) {
-      uint4 v = reinterpret_cast<const uint4*>(p)[i];
-      w[4 * i] = v.x; w[4 * i + 1] = v.y; w[4 * i + 2] = v.z; w[4 * i + 3] = v.w;
+      for (int i = 0; i < BC / 4; ++i) {
+        float4 v = reinterpret_cast<const float4*>(p)[i];
+        ffma2(acc[4 * i], acc[4 * i + 1], v.x, v.y, sg);
+        ffma2(acc[4 * i + 2], acc[4 * i + 3], v.z, v.w, sg);
+      }
     }
   }
 }
 
-template <typename ET, int BC>
-__device__ __forceinline__ float entry_col(const uint32_t (&w)[EntryVec<ET, BC>::kWords], int c) {
+template <typename ET, int BC> __device__ __forceinline__ void store_entry(uint8_t* p, const float* v) {
   if constexpr (sizeof(ET) == 4) {
-    return __uint_as_float(w[c]);
+    if constexpr (BC == 1) *reinterpret_cast<float*>(p) = v[0];
+    else if constexpr (BC == 2) *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+    else
+#pragma unroll
+      for (int i = 0; i < BC / 4; ++i)
+        reinterpret_cast<float4*>(p)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
   } else {
-    uint32_t word = w[c >> 1];
-    __half h = __ushort_as_half((unsigned short)((c & 1) ? (word >> 16) : (word & 0xFFFF)));
-    return __half2float(h);
+    if constexpr (BC == 1) {
+      *reinterpret_cast<__half*>(p) = __float2half_rn(v[0]);
+    } else {
+      uint32_t w[BC / 2];
+#pragma unroll
+      for (int i = 0; i < BC / 2; ++i) {
+        __half2 h = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+        w[i] = *reinterpret_cast<uint32_t*>(&h);
+      }
+      if constexpr (BC == 2) *reinterpret_cast<uint32_t*>(p) = w[0];
+      else if constexpr (BC == 4) *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
+      else *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
   }
 }
 
-template <typename ET> __device__ __forceinline__ void store_entries(uint8_t* p, const float* v, int n);
+// stored index of group g (0..3) from the quad words
+template <int D>
+__device__ __forceinline__ uint32_t stored_index(uint32_t lo, uint32_t hi, int g) {
+  if constexpr (D == 1) return (lo >> (4 * g)) & 0xF;
+  else if constexpr (D == 2) return (lo >> (8 * g)) & 0xFF;
+  else return ((lo >> (8 * g)) & 0xFF) | (((hi >> (4 * g)) & 0xF) << 8);
+}
+
+// Table layout: the 4 tables of a quad are interleaved in 128-byte rows, each
+// group owning a 32-byte slice (= 8 banks) of every row; entry f of group g
+// sits at row f / SPG, slot f % SPG of that slice.  Lanes reading different
+// groups therefore never share a bank.
+template <int EB> struct TabLayout {
+  static constexpr int SPG = 32 / EB;  // entries per group per 128-byte row
+  static constexpr int LSPG = SPG == 1 ? 0 : SPG == 2 ? 1 : SPG == 4 ? 2 : SPG == 8 ? 3 : 4;
+  static constexpr int LEB = EB == 2 ? 1 : EB == 4 ? 2 : EB == 8 ? 3 : EB == 16 ? 4 : 5;
+  static __device__ __forceinline__ uint32_t off(uint32_t f, uint32_t gslot) {
+    return ((f >> LSPG) << 7) | ((f & (SPG - 1)) << LEB) | gslot;
+  }
+};
+
+template <int D> struct FusedShape {
+  static constexpr int LOB = D == 1 ? 2 : 4;   // lo plane bytes per (quad,row)
+  static constexpr int HIB = D == 3 ? 2 : 0;   // hi plane bytes per (quad,row)
+};
 
 template <int D, typename XT, typename ET, int BC, bool SYM, int RPT>
 __global__ void __launch_bounds__(kThreads, 1) fused_lut_kernel(FusedParams P) {
@@ -178,18 +301,78 @@ __global__ void __launch_bounds__(kThreads, 1) fused_lut_kernel(FusedParams P) {
   constexpr int EB = BC * (int)sizeof(ET);                        // bytes per entry
   constexpr int LOWN = D == 1 ? 1 : (D == 2 ? 16 : 256);          // combos of the low D-1 codes
   constexpr int HIN = SYM ? 8 : 16;                               // values of the top code
-  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int R = kThreads * RPT;
+  constexpr int LOB = FusedShape<D>::LOB, HIB = FusedShape<D>::HIB;
+  constexpr int XPT = 2;  // staged activation values per thread (<= 512 per round)
+  constexpr int QUADB = 4 * ES * EB > 128 ? 4 * ES * EB : 128;  // table bytes per quad
+  using TL = TabLayout<EB>;
+  extern __shared__ __align__(128) uint8_t smem[];
 
   const int tid = threadIdx.x;
-  const int64_t row0 = (int64_t)blockIdx.x * kThreads * RPT;
+  const int64_t row0 = (int64_t)blockIdx.x * R;
   const int slice = blockIdx.y;
   const int64_t c0 = (int64_t)blockIdx.z * BC;
   const int64_t q_begin = (int64_t)slice * P.quads_per_slice;
-  const int64_t q_end = (P.nq < q_begin + P.quads_per_slice ? P.nq : q_begin + P.quads_per_slice);
+  const int64_t q_end = P.nq < q_begin + P.quads_per_slice ? P.nq : q_begin + P.quads_per_slice;
+  const int rows_valid = (int)((P.m - row0) < R ? (P.m - row0) : R);
+  const int rows_cp = (rows_valid + 7) & ~7;
+  const int QL = P.ql;
 
-  const int groups_cap = P.ql * 4;
-  uint8_t* tab = smem;                                              // [groups][ES][BC] ET
-  float* xs = reinterpret_cast<float*>(smem + (size_t)groups_cap * ES * EB);  // [groups*D][BC]
+  // ---- shared-memory carve-up
+  uint8_t* tab = smem;                                                   // [QL*4][ES][BC] ET
+  uint8_t* stage = tab + (size_t)QL * QUADB;                             // [2][QL][R] lo,hi
+  const size_t stage_bytes = (size_t)QL * R * (LOB + HIB);
+  float* xs = reinterpret_cast<float*>(stage + 2 * stage_bytes);         // [QL*4*D][BC]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(xs + QL * 4 * D * BC);   // [2]
+
+  const uint8_t* lo_plane = P.wrep + P.lo_off;
+  const uint8_t* hi_plane = P.wrep + P.hi_off;
+  const int nrounds = (int)((q_end - q_begin + QL - 1) / QL);
+
+  auto issue = [&](int t) {  // TMA bulk copies of round t's weight words (one thread)
+    const int64_t qa = q_begin + (int64_t)t * QL;
+    const int nql = (int)((q_end - qa) < QL ? (q_end - qa) : QL);
+    uint8_t* buf = stage + (t & 1) * stage_bytes;
+    uint64_t* bar = bars + (t & 1);
+    fence_proxy_async();
+    mbar_expect_tx(bar, (uint32_t)(nql * rows_cp * (LOB + HIB)));
+    for (int qq = 0; qq < nql; ++qq) {
+      const int64_t q = qa + qq;
+      bulk_g2s(buf + (size_t)qq * R * LOB, lo_plane + (q * P.mp + row0) * LOB,
+               (uint32_t)(rows_cp * LOB), bar);
+      if constexpr (HIB > 0)
+        bulk_g2s(buf + (size_t)QL * R * LOB + (size_t)qq * R * HIB,
+                 hi_plane + (q * P.mp + row0) * HIB, (uint32_t)(rows_cp * HIB), bar);
+    }
+  };
+  // activations of round t: element e -> (group row gr = e / BC, column c = e % BC)
+  auto load_x = [&](int t, float (&xv)[XPT]) {
+    const int64_t qa = q_begin + (int64_t)t * QL;
+    const int64_t g_first = qa * 4;
+    const int64_t qe = (qa + QL) < q_end ? (qa + QL) : q_end;
+    const int64_t glast = (qe * 4) < P.nb ? qe * 4 : P.nb;
+    const int nel = (int)(glast - g_first) * D * BC;
+#pragma unroll
+    for (int u = 0; u < XPT; ++u) {
+      const int e = tid + u * kThreads;
+      float v = 0.f;
+      if (e < nel) {
+        const int c = e % BC, gr = e / BC;
+        if (c0 + c < P.b) v = ldx<XT>(P.x, (g_first * D + gr) * P.b + c0 + c);
+      }
+      xv[u] = v;
+    }
+  };
+
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0 && nrounds > 0) issue(0);
+  float xnext[XPT];
+  if (nrounds > 0) load_x(0, xnext);
 
   float acc[RPT][BC];
 #pragma unroll
@@ -198,33 +381,40 @@ __global__ void __launch_bounds__(kThreads, 1) fused_lut_kernel(FusedParams P) {
     for (int c = 0; c < BC; ++c) acc[r][c] = 0.f;
   float corr = 0.f;  // thread tid < BC accumulates column tid's correction
 
-  const uint32_t* lo_plane = reinterpret_cast<const uint32_t*>(P.wrep + P.lo_off);
-  const uint16_t* lo16_plane = reinterpret_cast<const uint16_t*>(P.wrep + P.lo_off);
-  const uint16_t* hi_plane = reinterpret_cast<const uint16_t*>(P.wrep + P.hi_off);
+  float sv[HIN];
+#pragma unroll
+  for (int h = 0; h < HIN; ++h) sv[h] = P.s[h];
+  uint32_t gslot[4];  // table slice of the group at quad position g for this lane
+#pragma unroll
+  for (int g = 0; g < 4; ++g) gslot[g] = (uint32_t)((g + tid) & 3) << 5;
 
-  for (int64_t qa = q_begin; qa < q_end; qa += P.ql) {
-    const int nql = (int)((int64_t)P.ql < q_end - qa ? (int64_t)P.ql : q_end - qa);
+  for (int t = 0; t < nrounds; ++t) {
+    const int64_t qa = q_begin + (int64_t)t * QL;
+    const int nql = (int)((q_end - qa) < QL ? (q_end - qa) : QL);
     const int64_t g_first = qa * 4;
     const int ngroups = (int)((int64_t)nql * 4 < P.nb - g_first ? (int64_t)nql * 4 : P.nb - g_first);
 
-    __syncthreads();  // previous round's gathers are done with tab/xs
-    // ---- stage x for this round's groups: xs[gl*D + r][c] = x[(g*D + r), c0 + c]
-    for (int t = tid; t < ngroups * D * BC; t += kThreads) {
-      int c = t % BC, gr = t / BC;
-      int64_t col = c0 + c;
-      float v = 0.f;
-      if (col < P.b) v = ldx<XT>(P.x, (g_first * D + gr) * P.b + col);
-      xs[t] = v;
-    }
+    __syncthreads();  // round t-1 finished with tab, xs and stage[(t+1)&1]
+    if (tid == 0 && t + 1 < nrounds) issue(t + 1);
+#pragma unroll
+    for (int u = 0; u < XPT; ++u)
+      if (tid + u * kThreads < QL * 4 * D * BC) xs[tid + u * kThreads] = xnext[u];
+    if (t + 1 < nrounds) load_x(t + 1, xnext);
     __syncthreads();
     if (SYM && tid < BC) {
-      float s = 0.f;
-      for (int gr = 0; gr < ngroups * D; ++gr) s += xs[gr * BC + tid];
-      corr += s;
+      float sacc = 0.f;
+      for (int gr = 0; gr < ngroups * D; ++gr) sacc += xs[gr * BC + tid];
+      corr += sacc;
     }
-    // ---- build: entry(f) = sum_r s[nibble_r(f)] * x_r, top nibble < HIN
-    for (int t = tid; t < ngroups * LOWN; t += kThreads) {
-      const int gl = t / LOWN, low = t - gl * LOWN;
+    // ---- build: entry(f) = sum_r s[nibble_r(f)] * x_r, top nibble < HIN.
+    // Work item w -> (quad, group g = w % 4, low = (w / 4) % LOWN): the lanes of
+    // one store wavefront fill one whole 128-byte table row (4 groups x SPG
+    // consecutive entries), so the interleaved layout is written conflict-free.
+    for (int w = tid; w < nql * 4 * LOWN; w += kThreads) {
+      const int qq = w / (4 * LOWN), rem = w - qq * 4 * LOWN;
+      const int g = rem & 3, low = rem >> 2;
+      const int gl = qq * 4 + g;
+      if (gl >= ngroups) continue;
       const float* xg = xs + gl * D * BC;
       float base[BC];
 #pragma unroll
@@ -235,47 +425,75 @@ __global__ void __launch_bounds__(kThreads, 1) fused_lut_kernel(FusedParams P) {
         base[c] = v;
       }
       const float* xt = xg + (D - 1) * BC;
-      uint8_t* dst = tab + ((size_t)gl * ES + low) * EB;
-#pragma unroll 4
+      float xtop[BC];
+#pragma unroll
+      for (int c = 0; c < BC; ++c) xtop[c] = xt[c];
+      uint8_t* dst = tab + (size_t)qq * QUADB;
+      const uint32_t gslot_b = (uint32_t)g << 5;
+#pragma unroll
       for (int h = 0; h < HIN; ++h) {
         float e[BC];
-        const float sh = P.s[h];
+        if constexpr (BC == 1) {
+          e[0] = fmaf(sv[h], xtop[0], base[0]);
+        } else {
 #pragma unroll
-        for (int c = 0; c < BC; ++c) e[c] = fmaf(sh, xt[c], base[c]);
-        store_entries<ET>(dst + (size_t)h * LOWN * EB, e, BC);
+          for (int c = 0; c < BC; c += 2)
+            fma2_to(e[c], e[c + 1], sv[h], xtop[c], xtop[c + 1], base[c], base[c + 1]);
+        }
+        store_entry<ET, BC>(dst + TL::off((uint32_t)(low + h * LOWN), gslot_b), e);
       }
     }
     __syncthreads();
+    mbar_wait(&bars[t & 1], (uint32_t)((t >> 1) & 1));
     // ---- gather
+    const uint8_t* buf = stage + (t & 1) * stage_bytes;
+    for (int qq = 0; qq < nql; ++qq) {
+      const uint8_t* lo_s = buf + (size_t)qq * R * LOB;
+      const uint16_t* hi_s =
+          reinterpret_cast<const uint16_t*>(buf + (size_t)QL * R * LOB + (size_t)qq * R * HIB);
+      const uint8_t* tq = tab + (size_t)qq * QUADB;
+      const int gcount = ngroups - qq * 4;
+      if (gcount >= 4) {
 #pragma unroll
-    for (int r = 0; r < RPT; ++r) {
-      const int64_t i = row0 + (int64_t)r * kThreads + tid;
-      if (i < P.m) {
-        for (int qq = 0; qq < nql; ++qq) {
-          const int64_t q = qa + qq;
-          uint32_t lo, hi = 0;
-          if constexpr (D == 1) lo = lo16_plane[q * P.m + i];
-          else lo = __ldg(lo_plane + q * P.m + i);
-          if constexpr (D == 3) hi = hi_plane[q * P.m + i];
-          const int gbase = qq * 4;
-          const int gmax = min(4, ngroups - gbase);
+        for (int r = 0; r < RPT; ++r) {
+          const int li = r * kThreads + tid;
+          if (li < rows_valid) {
+            uint32_t lo, hi = 0;
+            if constexpr (LOB == 4) lo = reinterpret_cast<const uint32_t*>(lo_s)[li];
+            else lo = reinterpret_cast<const uint16_t*>(lo_s)[li];
+            if constexpr (HIB > 0) hi = hi_s[li];
 #pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            if (g < gmax) {
-              uint32_t st;
-              if constexpr (D == 1) st = (lo >> (4 * g)) & 0xF;
-              else if constexpr (D == 2) st = (lo >> (8 * g)) & 0xFF;
-              else st = ((lo >> (8 * g)) & 0xFF) | (((hi >> (4 * g)) & 0xF) << 8);
-              float sg = 1.f;
+            for (int g = 0; g < 4; ++g) {
+              const uint32_t st = stored_index<D>(lo, hi, g);
               uint32_t f = st;
+              float sg = 1.f;
               if constexpr (SYM) {
                 f = st & (ES - 1);
                 sg = (st & ES) ? -1.f : 1.f;
               }
-              uint32_t w[EntryVec<ET, BC>::kWords];
-              load_entry<ET, BC>(tab + ((size_t)(gbase + g) * ES + f) * EB, w);
+              gather_acc<ET, BC>(tq + TL::off(f, gslot[g]), sg, acc[r]);
+            }
+          }
+        }
+      } else {
 #pragma unroll
-              for (int c = 0; c < BC; ++c) acc[r][c] = fmaf(sg, entry_col<ET, BC>(w, c), acc[r][c]);
+        for (int r = 0; r < RPT; ++r) {
+          const int li = r * kThreads + tid;
+          if (li < rows_valid) {
+            uint32_t lo, hi = 0;
+            if constexpr (LOB == 4) lo = reinterpret_cast<const uint32_t*>(lo_s)[li];
+            else lo = reinterpret_cast<const uint16_t*>(lo_s)[li];
+            if constexpr (HIB > 0) hi = hi_s[li];
+            for (int g = 0; g < 4; ++g) {
+              if (((g + tid) & 3) >= gcount) continue;
+              const uint32_t st = stored_index<D>(lo, hi, g);
+              uint32_t f = st;
+              float sg = 1.f;
+              if constexpr (SYM) {
+                f = st & (ES - 1);
+                sg = (st & ES) ? -1.f : 1.f;
+              }
+              gather_acc<ET, BC>(tq + TL::off(f, gslot[g]), sg, acc[r]);
             }
           }
         }
@@ -285,34 +503,22 @@ __global__ void __launch_bounds__(kThreads, 1) fused_lut_kernel(FusedParams P) {
   // ---- write partials [slice][i][c]
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {
-    const int64_t i = row0 + (int64_t)r * kThreads + tid;
-    if (i < P.m) {
-      float* dst = P.partial + ((int64_t)slice * P.m + i) * P.b + c0;
+    const int li = r * kThreads + tid;
+    if (li < rows_valid) {
+      float* dst = P.partial + ((int64_t)slice * P.m + row0 + li) * P.b + c0;
+      if (c0 + BC <= P.b && BC >= 2 && (P.b % 2 == 0)) {
 #pragma unroll
-      for (int c = 0; c < BC; ++c)
-        if (c0 + c < P.b) dst[c] = acc[r][c];
+        for (int c = 0; c < BC; c += 2)
+          *reinterpret_cast<float2*>(dst + c) = make_float2(acc[r][c], acc[r][c + 1]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < BC; ++c)
+          if (c0 + c < P.b) dst[c] = acc[r][c];
+      }
     }
   }
   if (SYM && blockIdx.x == 0 && tid < BC && c0 + tid < P.b)
     P.corr[(int64_t)slice * P.b + c0 + tid] = P.beta * corr;
-}
-
-template <> __device__ __forceinline__ void store_entries<float>(uint8_t* p, const float* v, int n) {
-  if (n == 1) { *reinterpret_cast<float*>(p) = v[0]; return; }
-  if (n == 2) { *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]); return; }
-  for (int i = 0; i < n; i += 4)
-    reinterpret_cast<float4*>(p)[i / 4] = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-}
-template <> __device__ __forceinline__ void store_entries<__half>(uint8_t* p, const float* v, int n) {
-  if (n == 1) { *reinterpret_cast<__half*>(p) = __float2half_rn(v[0]); return; }
-  uint32_t w[4];
-  for (int i = 0; i < n / 2; ++i) {
-    __half2 h = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
-    w[i] = *reinterpret_cast<uint32_t*>(&h);
-  }
-  if (n == 2) { *reinterpret_cast<uint32_t*>(p) = w[0]; return; }
-  if (n == 4) { *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]); return; }
-  *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
 // ============================================================================
@@ -322,6 +528,9 @@ struct TailVals {
   float v[16];
 };
 
+// LPO lanes cooperate on one output: lane j sums slices j, j+LPO, ... in order,
+// then a fixed butterfly combines them -- deterministic run to run.
+template <int LPO>
 __global__ void fused_finish_kernel(const float* __restrict__ partial,
                                     const float* __restrict__ corr, int S, int64_t m, int64_t b,
                                     int64_t k, int d, const uint16_t* __restrict__ tailp,
@@ -331,20 +540,33 @@ __global__ void fused_finish_kernel(const float* __restrict__ partial,
   const int64_t nb = k / d;
   const int tail = (int)(k - nb * d);
   const int64_t total = m * b;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t i = t / b, c = t - i * b;
+  const int lane = threadIdx.x % LPO;
+  const int64_t per_block = blockDim.x / LPO;
+  for (int64_t t0 = (int64_t)blockIdx.x * per_block; t0 < total;
+       t0 += (int64_t)gridDim.x * per_block) {
+    const int64_t t = t0 + threadIdx.x / LPO;
     float s = 0.f;
-    for (int sl = 0; sl < S; ++sl) s += partial[(int64_t)sl * total + t];
-    if (corr)
-      for (int sl = 0; sl < S; ++sl) s += corr[(int64_t)sl * b + c];
-    if (tail) {
-      uint32_t tc = tailp[i];
-      for (int u = 0; u < tail; ++u)
-        s = fmaf(vals.v[(tc >> (4 * u)) & 0xF], load_as<float>(x, x_dtype, (nb * d + u) * b + c), s);
+    if (t < total) {
+      int sl = lane;
+#pragma unroll 4
+      for (; sl < S; sl += LPO) s += partial[(int64_t)sl * total + t];
     }
-    if (scale_mode == MSG_SCALE_PER_ROW) s *= load_as<float>(q, q_dtype, i);
-    store_as<float>(y, y_dtype, t, s);
+    if constexpr (LPO > 1) {
+#pragma unroll
+      for (int o = LPO / 2; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, LPO);
+    }
+    if (t < total && lane == 0) {
+      const int64_t i = t / b, c = t - i * b;
+      if (corr)
+        for (int sl = 0; sl < S; ++sl) s += corr[(int64_t)sl * b + c];
+      if (tail) {
+        uint32_t tc = tailp[i];
+        for (int u = 0; u < tail; ++u)
+          s = fmaf(vals.v[(tc >> (4 * u)) & 0xF], load_as<float>(x, x_dtype, (nb * d + u) * b + c), s);
+      }
+      if (scale_mode == MSG_SCALE_PER_ROW) s *= load_as<float>(q, q_dtype, i);
+      store_as<float>(y, y_dtype, t, s);
+    }
   }
 }
 
@@ -372,6 +594,8 @@ static bool fused_eligible(int width, int x_dtype, int d, int scale_mode) {
          scale_mode != MSG_SCALE_PER_GROUP;
 }
 
+static int rpt_for(int bc) { return bc == 8 ? 16 : 32; }
+
 static FusedPlan fused_plan(int64_t m, int64_t k, int width, const double* values, int x_dtype,
                             int64_t b, int d, int scale_mode, int flags) {
   FusedPlan p{};
@@ -384,17 +608,20 @@ static FusedPlan fused_plan(int64_t m, int64_t k, int width, const double* value
   p.f32_entries = (x_dtype == MSG_F32) || (flags & MSG_FLAG_F32_ENTRIES);
   const int esize = p.f32_entries ? 4 : 2;
   const int64_t ES = p.sym ? (1 << (4 * d - 1)) : (1 << (4 * d));
-  const int64_t budget = std::min<int64_t>(max_smem_optin(), 227 * 1024) - 8 * 1024;
+  const int64_t budget = std::min<int64_t>(max_smem_optin(), 227 * 1024) - 2 * 1024;
+  const int lob = d == 1 ? 2 : 4, hib = d == 3 ? 2 : 0;
   int bc = b >= 8 ? 8 : (b >= 4 ? 4 : (b >= 2 ? 2 : 1));
   if (b == 3) bc = 4;
   if (b > 4 && b < 8) bc = 8;
-  // shrink the column tile until one quad of tables fits
-  while (bc > 1 && 4 * ES * bc * esize > budget) bc /= 2;
-  if (4 * ES * bc * esize > budget) return p;
+  auto quad_bytes = [&](int bcx) {  // tables + 2 staging buffers + staged x, per quad
+    return std::max<int64_t>(4 * ES * bcx * esize, 128) +
+           2 * (int64_t)kThreads * rpt_for(bcx) * (lob + hib) + 4 * d * bcx * 4;
+  };
+  while (bc > 1 && quad_bytes(bc) > budget) bc /= 2;
+  if (quad_bytes(bc) > budget) return p;
   p.bc = bc;
-  p.rpt = bc == 8 ? 16 : 32;
+  p.rpt = rpt_for(bc);
   p.L = quad_layout(m, k, d);
-  const int64_t quad_bytes = 4 * ES * bc * esize + 4 * d * bc * 4;  // tables + staged x
   p.nrow_blocks = (int)ceil_div(m, (int64_t)kThreads * p.rpt);
   p.ncol_tiles = (int)ceil_div(b, bc);
   const int64_t base = (int64_t)p.nrow_blocks * p.ncol_tiles;
@@ -402,8 +629,11 @@ static FusedPlan fused_plan(int64_t m, int64_t k, int width, const double* value
   S = std::min<int64_t>(S, p.L.nq);
   p.quads_per_slice = (int)ceil_div(p.L.nq, S);
   p.S = (int)ceil_div(p.L.nq, p.quads_per_slice);
-  p.ql = (int)std::max<int64_t>(1, std::min<int64_t>(budget / quad_bytes, p.quads_per_slice));
-  p.smem = p.ql * quad_bytes;
+  int64_t ql = std::max<int64_t>(1, std::min<int64_t>(budget / quad_bytes(bc), p.quads_per_slice));
+  // staged activations: at most 2 per thread per round
+  while (ql > 1 && ql * 4 * d * bc > 2 * kThreads) --ql;
+  p.ql = (int)ql;
+  p.smem = p.ql * quad_bytes(bc) + 16;
   p.partial_bytes = align256((int64_t)p.S * m * b * 4);
   p.corr_bytes = align256((int64_t)p.S * b * 4);
   p.ok = true;
@@ -471,14 +701,9 @@ int msg_repack(const uint8_t* packed, int64_t m, int64_t k, int d, int layout, i
     return fail(MSG_ERR_UNSUPPORTED, "unknown weight layout %d", layout);
   if (d < 1 || d > 3) return fail(MSG_ERR_UNSUPPORTED, "quad layout supports d in 1..3, got %d", d);
   QuadLayout L = quad_layout(m, k, d);
-  int64_t total = L.nq * m;
-  if (total == 0 && !(L.tail && m)) return MSG_OK;
-  int64_t n = std::max<int64_t>(total, 1);
-  int grid = (int)std::min<int64_t>(ceil_div(n, 256), (int64_t)sm_count() * 16);
-  if (total == 0) {
-    // k < d: only a tail plane; handled by a degenerate launch over rows
-    return fail(MSG_ERR_UNSUPPORTED, "quad layout needs at least one full group");
-  }
+  int64_t total = L.nq * L.mp;
+  if (total == 0) return fail(MSG_ERR_UNSUPPORTED, "quad layout needs at least one full group");
+  int grid = (int)std::min<int64_t>(ceil_div(total, 256), (int64_t)sm_count() * 16);
   repack_quad_kernel<<<grid, 256, 0, as_stream(stream)>>>(packed, m, k, d, row_bytes(k, 4),
                                                          symmetric, L, out);
   MSG_LAUNCH_CHECK();
@@ -544,12 +769,12 @@ int msg_gemm(const uint8_t* packed, const uint8_t* wrep, int64_t m, int64_t k, i
   P.wrep = wrep;
   P.lo_off = p.L.lo_off;
   P.hi_off = p.L.hi_off;
+  P.mp = p.L.mp;
   P.m = m;
   P.nb = p.L.nb;
   P.nq = p.L.nq;
   P.x = x;
   P.b = b;
-  P.d = d;
   for (int c = 0; c < 16; ++c) P.s[c] = (float)(values[c] - beta);
   P.beta = (float)beta;
   P.quads_per_slice = p.quads_per_slice;
@@ -567,12 +792,26 @@ int msg_gemm(const uint8_t* packed, const uint8_t* wrep, int64_t m, int64_t k, i
   TailVals tv;
   for (int c = 0; c < 16; ++c) tv.v[c] = (float)values[c];
   const int64_t total = m * b;
-  const int grid = (int)std::min<int64_t>(ceil_div(total, 256), (int64_t)sm_count() * 8);
   const uint16_t* tailp =
       p.L.tail ? reinterpret_cast<const uint16_t*>(wrep + p.L.tail_off) : nullptr;
-  fused_finish_kernel<<<grid, 256, 0, s>>>(P.partial, p.sym ? P.corr : nullptr, p.S, m, b, k, d,
-                                           tailp, tv, x, x_dtype, scale_mode, q, q_dtype, y,
-                                           y_dtype);
+  // lanes per output: enough threads to cover the SMs, never more than slices
+  int lpo = 1;
+  while (lpo < 32 && lpo < p.S && total * lpo < (int64_t)sm_count() * 1024) lpo *= 2;
+  const int grid =
+      (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total * lpo, 256), (int64_t)sm_count() * 8));
+  const float* corr = p.sym ? P.corr : nullptr;
+#define MSG_FIN(L)                                                                            \
+  fused_finish_kernel<L><<<grid, 256, 0, s>>>(P.partial, corr, p.S, m, b, k, d, tailp, tv, x, \
+                                              x_dtype, scale_mode, q, q_dtype, y, y_dtype)
+  switch (lpo) {
+    case 1: MSG_FIN(1); break;
+    case 2: MSG_FIN(2); break;
+    case 4: MSG_FIN(4); break;
+    case 8: MSG_FIN(8); break;
+    case 16: MSG_FIN(16); break;
+    default: MSG_FIN(32); break;
+  }
+#undef MSG_FIN
   MSG_LAUNCH_CHECK();
   return MSG_OK;
 }
