@@ -69,12 +69,18 @@ extern "C" {
 #define MSG_FLAG_NO_SYMMETRY   2  /* full 16^d tables (default: sign-symmetric half tables) */
 #define MSG_FLAG_FORCE_GENERIC 4  /* global-memory table path (any d, width, dtype)        */
 #define MSG_FLAG_LUT_PHASE_ONLY 8 /* measurement: launch only the fused LUT kernel (Y untouched) */
+#define MSG_FLAG_NO_LANE      16  /* do not use the b=1 lane kernel (use the row-block kernel) */
 
 /* weight layouts produced by msg_repack */
 #define MSG_LAYOUT_NONE 0  /* reference row-major nibbles only      */
 #define MSG_LAYOUT_QUAD 1  /* quad planes for the fused LUT kernel  */
+#define MSG_LAYOUT_LANE 2  /* lane-rotated 32-group chunks for the b=1, d=3 GEMV kernel */
 
 MSG_API const char* msg_last_error(void);
+/* diagnostics: per-CTA trace records {smid, t_start_ns, t_end_ns, units} of
+ * the LUT kernels launched while tracing is on (at most 4096, last launch) */
+MSG_API int msg_set_tracing(int on);
+MSG_API int msg_read_trace(uint64_t* host_records, int max_records);
 MSG_API int msg_version(void);
 MSG_API int msg_device_sm_count(void);
 

@@ -23,13 +23,14 @@ MSG_ERR_UNSUPPORTED, MSG_ERR_CUDA, MSG_ERR_WORKSPACE = -4, -5, -6
 F32, F16, F64, I32, I64, U8, I8, I16, BF16 = range(9)
 SCALE_NONE, SCALE_PER_ROW, SCALE_PER_GROUP = 0, 1, 2
 FLAG_F32_ENTRIES, FLAG_NO_SYMMETRY, FLAG_FORCE_GENERIC, FLAG_LUT_PHASE_ONLY = 1, 2, 4, 8
-LAYOUT_NONE, LAYOUT_QUAD = 0, 1
+FLAG_NO_LANE = 16
+LAYOUT_NONE, LAYOUT_QUAD, LAYOUT_LANE = 0, 1, 2
 
 EXPORTS = (
     "msg_last_error", "msg_version", "msg_device_sm_count", "msg_pack_codes",
     "msg_unpack_codes", "msg_group_indices", "msg_encode_values", "msg_lut_build",
     "msg_repacked_bytes", "msg_repack", "msg_gemm_plan", "msg_gemm",
-    "msg_dequant_mma_workspace_bytes", "msg_dequant_mma",
+    "msg_dequant_mma_workspace_bytes", "msg_dequant_mma", "msg_set_tracing", "msg_read_trace",
 )
 
 _c_i64 = ctypes.c_int64
@@ -54,6 +55,8 @@ _SIGS = {
     "msg_dequant_mma_workspace_bytes": (_c_i64, [_c_i64, _c_i64, _c_i64]),
     "msg_dequant_mma": (_c_int, [_vp, _c_i64, _c_i64, _vp, _vp, _c_i64, _vp, _vp, _c_i64,
                                  _vp]),
+    "msg_set_tracing": (_c_int, [_c_int]),
+    "msg_read_trace": (_c_int, [_vp, _c_int]),
 }
 
 _lib = None
@@ -193,3 +196,13 @@ def workspace(nbytes: int, dev):
         buf = t.empty(max(int(nbytes), 256), dtype=t.uint8, device=dev)
         _ws[key] = buf
     return buf
+
+
+def read_trace(max_records: int = 4096):
+    """Per-CTA trace records (smid, t0_ns, t1_ns, units) of the last traced launch."""
+    buf = (ctypes.c_uint64 * (4 * max_records))()
+    n = lib().msg_read_trace(buf, max_records)
+    if n < 0:
+        check(n)
+    a = np.frombuffer(buf, dtype=np.uint64).reshape(max_records, 4)[:n]
+    return a[a[:, 2] > 0]

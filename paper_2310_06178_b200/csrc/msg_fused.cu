@@ -41,6 +41,15 @@ int run_generic(const uint8_t* packed, int64_t m, int64_t k, int width, const Co
                 const void* q, int q_dtype, void* y, int y_dtype, void* ws, int64_t ws_bytes,
                 cudaStream_t s);
 int64_t generic_workspace_bytes(int64_t m, int64_t k, int width, int x_dtype, int64_t b, int d);
+// b = 1 GEMV kernel (msg_lane.cu)
+bool lane_eligible(int width, int x_dtype, int64_t b, int d, int scale_mode, bool sym,
+                   bool f32_entries);
+int64_t lane_layout_bytes(int64_t m, int64_t k);
+int64_t lane_tail_offset(int64_t m, int64_t k);
+int64_t lane_partial_slices(int64_t m, int64_t k);
+int lane_repack(const uint8_t* packed, int64_t m, int64_t k, uint8_t* out, cudaStream_t s);
+int launch_lane(const uint8_t* wrep, int64_t m, int64_t k, const double* values, double beta,
+                const void* x, int x_dtype, float* partial, cudaStream_t s);
 
 static inline int64_t align256(int64_t v) { return (v + 255) / 256 * 256; }
 
@@ -118,41 +127,6 @@ __global__ void repack_quad_kernel(const uint8_t* __restrict__ packed, int64_t m
 // ============================================================================
 // async-copy and packed-math helpers (PTX)
 // ============================================================================
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void fence_mbar_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
-                                         uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
 // a0,a1 += x0*s, x1*s  (one FFMA2)
 __device__ __forceinline__ void ffma2(float& a0, float& a1, float x0, float x1, float s) {
   unsigned long long acc, xv, sv;
@@ -189,7 +163,6 @@ struct FusedParams {
   int quads_per_slice;  // k-slice length in quads
   int ql;               // quads per table round
   float* partial;       // [S][m][b]
-  float* corr;          // [S][b]   beta * sum of x over the slice (symmetric only)
 };
 
 template <typename XT> __device__ __forceinline__ float ldx(const void* p, int64_t i);
@@ -207,27 +180,43 @@ __device__ __forceinline__ float h2f_hi(uint32_t w) {
   return __half2float(__ushort_as_half((unsigned short)(w >> 16)));
 }
 
-// acc[0..BC) += sg * entry (BC values of type ET at p)
-template <typename ET, int BC>
-__device__ __forceinline__ void gather_acc(const uint8_t* p, float sg, float* acc) {
+// acc += h * s16 with h, s16 fp16 and acc fp32 (sm_100 FHFMA: one instruction,
+// no separate f16->f32 conversion; the product is exact, one fp32 rounding)
+__device__ __forceinline__ void fhfma(float& acc, unsigned short h, unsigned short s16) {
+  asm("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(acc) : "h"(h), "h"(s16));
+}
+__device__ __forceinline__ void fhfma2w(float& a0, float& a1, uint32_t w, unsigned short s16) {
+  unsigned short h0, h1;
+  asm("mov.b32 {%0, %1}, %2;" : "=h"(h0), "=h"(h1) : "r"(w));
+  fhfma(a0, h0, s16);
+  fhfma(a1, h1, s16);
+}
+
+// acc[0..BC) += sign * entry (BC values of type ET at p); the sign is bit
+// SBIT of the stored index st (symmetric tables) or +1.
+template <typename ET, int BC, bool SYM, int SBIT>
+__device__ __forceinline__ void gather_acc(const uint8_t* p, uint32_t st, float* acc) {
   if constexpr (sizeof(ET) == 2) {
+    unsigned short s16 = 0x3C00;  // +1.0h
+    if constexpr (SYM) s16 = (unsigned short)(0x3C00 | ((st >> SBIT) << 15));
     if constexpr (BC == 1) {
-      acc[0] = fmaf(sg, __half2float(*reinterpret_cast<const __half*>(p)), acc[0]);
+      fhfma(acc[0], *reinterpret_cast<const unsigned short*>(p), s16);
     } else if constexpr (BC == 2) {
-      uint32_t w = *reinterpret_cast<const uint32_t*>(p);
-      ffma2(acc[0], acc[1], h2f_lo(w), h2f_hi(w), sg);
+      fhfma2w(acc[0], acc[1], *reinterpret_cast<const uint32_t*>(p), s16);
     } else if constexpr (BC == 4) {
       uint2 v = *reinterpret_cast<const uint2*>(p);
-      ffma2(acc[0], acc[1], h2f_lo(v.x), h2f_hi(v.x), sg);
-      ffma2(acc[2], acc[3], h2f_lo(v.y), h2f_hi(v.y), sg);
+      fhfma2w(acc[0], acc[1], v.x, s16);
+      fhfma2w(acc[2], acc[3], v.y, s16);
     } else {
       uint4 v = *reinterpret_cast<const uint4*>(p);
-      ffma2(acc[0], acc[1], h2f_lo(v.x), h2f_hi(v.x), sg);
-      ffma2(acc[2], acc[3], h2f_lo(v.y), h2f_hi(v.y), sg);
-      ffma2(acc[4], acc[5], h2f_lo(v.z), h2f_hi(v.z), sg);
-      ffma2(acc[6], acc[7], h2f_lo(v.w), h2f_hi(v.w), sg);
+      fhfma2w(acc[0], acc[1], v.x, s16);
+      fhfma2w(acc[2], acc[3], v.y, s16);
+      fhfma2w(acc[4], acc[5], v.z, s16);
+      fhfma2w(acc[6], acc[7], v.w, s16);
     }
   } else {
+    float sg = 1.f;
+    if constexpr (SYM) sg = ((st >> SBIT) & 1) ? -1.f : 1.f;
     if constexpr (BC == 1) {
       acc[0] = fmaf(sg, *reinterpret_cast<const float*>(p), acc[0]);
     } else if constexpr (BC == 2) {
@@ -465,13 +454,8 @@ __global__ void __launch_bounds__(kThreads, 1) fused_lut_kernel(FusedParams P) {
 #pragma unroll
             for (int g = 0; g < 4; ++g) {
               const uint32_t st = stored_index<D>(lo, hi, g);
-              uint32_t f = st;
-              float sg = 1.f;
-              if constexpr (SYM) {
-                f = st & (ES - 1);
-                sg = (st & ES) ? -1.f : 1.f;
-              }
-              gather_acc<ET, BC>(tq + TL::off(f, gslot[g]), sg, acc[r]);
+              const uint32_t f = SYM ? (st & (ES - 1)) : st;
+              gather_acc<ET, BC, SYM, 4 * D - 1>(tq + TL::off(f, gslot[g]), st, acc[r]);
             }
           }
         }
@@ -487,18 +471,26 @@ __global__ void __launch_bounds__(kThreads, 1) fused_lut_kernel(FusedParams P) {
             for (int g = 0; g < 4; ++g) {
               if (((g + tid) & 3) >= gcount) continue;
               const uint32_t st = stored_index<D>(lo, hi, g);
-              uint32_t f = st;
-              float sg = 1.f;
-              if constexpr (SYM) {
-                f = st & (ES - 1);
-                sg = (st & ES) ? -1.f : 1.f;
-              }
-              gather_acc<ET, BC>(tq + TL::off(f, gslot[g]), sg, acc[r]);
+              const uint32_t f = SYM ? (st & (ES - 1)) : st;
+              gather_acc<ET, BC, SYM, 4 * D - 1>(tq + TL::off(f, gslot[g]), st, acc[r]);
             }
           }
         }
       }
     }
+  }
+  // ---- fold this slice's symmetry correction beta * sum(x) into every row
+  if constexpr (SYM) {
+    __syncthreads();
+    if (tid < BC) xs[tid] = P.beta * corr;
+    __syncthreads();
+    float cv[BC];
+#pragma unroll
+    for (int c = 0; c < BC; ++c) cv[c] = xs[c];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r)
+#pragma unroll
+      for (int c = 0; c < BC; ++c) acc[r][c] += cv[c];
   }
   // ---- write partials [slice][i][c]
 #pragma unroll
@@ -517,8 +509,6 @@ __global__ void __launch_bounds__(kThreads, 1) fused_lut_kernel(FusedParams P) {
       }
     }
   }
-  if (SYM && blockIdx.x == 0 && tid < BC && c0 + tid < P.b)
-    P.corr[(int64_t)slice * P.b + c0 + tid] = P.beta * corr;
 }
 
 // ============================================================================
@@ -532,7 +522,7 @@ struct TailVals {
 // then a fixed butterfly combines them -- deterministic run to run.
 template <int LPO>
 __global__ void fused_finish_kernel(const float* __restrict__ partial,
-                                    const float* __restrict__ corr, int S, int64_t m, int64_t b,
+                                    int S, int64_t m, int64_t b,
                                     int64_t k, int d, const uint16_t* __restrict__ tailp,
                                     TailVals vals, const void* x, int x_dtype,
                                     int scale_mode, const void* q, int q_dtype, void* y,
@@ -557,8 +547,6 @@ __global__ void fused_finish_kernel(const float* __restrict__ partial,
     }
     if (t < total && lane == 0) {
       const int64_t i = t / b, c = t - i * b;
-      if (corr)
-        for (int sl = 0; sl < S; ++sl) s += corr[(int64_t)sl * b + c];
       if (tail) {
         uint32_t tc = tailp[i];
         for (int u = 0; u < tail; ++u)
@@ -574,10 +562,10 @@ __global__ void fused_finish_kernel(const float* __restrict__ partial,
 // host planning / dispatch
 // ============================================================================
 struct FusedPlan {
-  bool ok;
+  bool ok, lane;
   int bc, rpt, ql, S, nrow_blocks, ncol_tiles, quads_per_slice;
   bool sym, f32_entries;
-  int64_t smem, partial_bytes, corr_bytes;
+  int64_t smem, partial_bytes;
   QuadLayout L;
 };
 
@@ -606,6 +594,14 @@ static FusedPlan fused_plan(int64_t m, int64_t k, int width, const double* value
   double beta = 0;
   p.sym = !(flags & MSG_FLAG_NO_SYMMETRY) && codebook_antisymmetric(values, 16, &beta);
   p.f32_entries = (x_dtype == MSG_F32) || (flags & MSG_FLAG_F32_ENTRIES);
+  if (!(flags & MSG_FLAG_NO_LANE) &&
+      lane_eligible(width, x_dtype, b, d, scale_mode, p.sym, p.f32_entries)) {
+    p.lane = true;
+    p.S = (int)lane_partial_slices(m, k);
+    p.partial_bytes = align256((int64_t)p.S * m * 4);
+    p.ok = true;
+    return p;
+  }
   const int esize = p.f32_entries ? 4 : 2;
   const int64_t ES = p.sym ? (1 << (4 * d - 1)) : (1 << (4 * d));
   const int64_t budget = std::min<int64_t>(max_smem_optin(), 227 * 1024) - 2 * 1024;
@@ -635,7 +631,6 @@ static FusedPlan fused_plan(int64_t m, int64_t k, int width, const double* value
   p.ql = (int)ql;
   p.smem = p.ql * quad_bytes(bc) + 16;
   p.partial_bytes = align256((int64_t)p.S * m * b * 4);
-  p.corr_bytes = align256((int64_t)p.S * b * 4);
   p.ok = true;
   return p;
 }
@@ -683,6 +678,11 @@ static int launch_fused_d(const FusedPlan& pl, FusedParams& P, int x_dtype, cuda
   return launch_fused_xt<D, float>(pl, P, s);
 }
 
+int launch_finish(const float* partial, int S, int64_t m, int64_t b, int64_t k, int d,
+                  const uint16_t* tailp, const TailVals& tv, const void* x, int x_dtype,
+                  int scale_mode, const void* q, int q_dtype, void* y, int y_dtype,
+                  cudaStream_t s);
+
 }  // namespace msg
 
 using namespace msg;
@@ -691,12 +691,18 @@ extern "C" {
 
 int64_t msg_repacked_bytes(int64_t m, int64_t k, int d, int layout) {
   if (layout == MSG_LAYOUT_NONE) return 0;
+  if (layout == MSG_LAYOUT_LANE) return d == 3 ? lane_layout_bytes(m, k) : -1;
   if (layout != MSG_LAYOUT_QUAD || d < 1 || d > 3) return -1;
   return quad_layout(m, k, d).total;
 }
 
 int msg_repack(const uint8_t* packed, int64_t m, int64_t k, int d, int layout, int symmetric,
                uint8_t* out, void* stream) {
+  if (layout == MSG_LAYOUT_LANE) {
+    if (d != 3 || !symmetric)
+      return fail(MSG_ERR_UNSUPPORTED, "lane layout is for d=3 with an antisymmetric codebook");
+    return lane_repack(packed, m, k, out, as_stream(stream));
+  }
   if (layout != MSG_LAYOUT_QUAD)
     return fail(MSG_ERR_UNSUPPORTED, "unknown weight layout %d", layout);
   if (d < 1 || d > 3) return fail(MSG_ERR_UNSUPPORTED, "quad layout supports d in 1..3, got %d", d);
@@ -736,9 +742,9 @@ int msg_gemm_plan(int64_t m, int64_t k, int width, const double* values, int x_d
   if (int e = validate_gemm(m, k, width, x_dtype, b, d, scale_mode, group_size)) return e;
   FusedPlan p = fused_plan(m, k, width, values, x_dtype, b, d, scale_mode, flags);
   if (p.ok) {
-    *layout_out = MSG_LAYOUT_QUAD;
+    *layout_out = p.lane ? MSG_LAYOUT_LANE : MSG_LAYOUT_QUAD;
     *symmetric_out = p.sym ? 1 : 0;
-    *ws_out = p.partial_bytes + p.corr_bytes;
+    *ws_out = p.partial_bytes;
   } else {
     *layout_out = MSG_LAYOUT_NONE;
     *symmetric_out = 0;
@@ -760,11 +766,22 @@ int msg_gemm(const uint8_t* packed, const uint8_t* wrep, int64_t m, int64_t k, i
     return run_generic(packed, m, k, width, cb, x, x_dtype, b, d, scale_mode, group_size, q,
                        q_dtype, y, y_dtype, workspace, ws_bytes, s);
   if (!wrep) return fail(MSG_ERR_VALUE, "fused path needs the repacked (quad) weight layout");
-  if (ws_bytes < p.partial_bytes + p.corr_bytes)
+  if (ws_bytes < p.partial_bytes)
     return fail(MSG_ERR_WORKSPACE, "workspace too small: need %lld bytes",
-                (long long)(p.partial_bytes + p.corr_bytes));
+                (long long)(p.partial_bytes));
   double beta = 0;
   if (p.sym) codebook_antisymmetric(values, 16, &beta);
+  TailVals tv;
+  for (int c = 0; c < 16; ++c) tv.v[c] = (float)values[c];
+  float* partial = reinterpret_cast<float*>(workspace);
+  if (p.lane) {
+    if (int e = launch_lane(wrep, m, k, values, beta, x, x_dtype, partial, s)) return e;
+    if (flags & MSG_FLAG_LUT_PHASE_ONLY) return MSG_OK;
+    const uint16_t* tailp =
+        (k % 3) ? reinterpret_cast<const uint16_t*>(wrep + lane_tail_offset(m, k)) : nullptr;
+    return launch_finish(partial, p.S, m, 1, k, d, tailp, tv, x, x_dtype, scale_mode, q, q_dtype,
+                         y, y_dtype, s);
+  }
   FusedParams P{};
   P.wrep = wrep;
   P.lo_off = p.L.lo_off;
@@ -780,7 +797,6 @@ int msg_gemm(const uint8_t* packed, const uint8_t* wrep, int64_t m, int64_t k, i
   P.quads_per_slice = p.quads_per_slice;
   P.ql = p.ql;
   P.partial = reinterpret_cast<float*>(workspace);
-  P.corr = reinterpret_cast<float*>((char*)workspace + p.partial_bytes);
   int e = MSG_OK;
   switch (d) {
     case 1: e = launch_fused_d<1>(p, P, x_dtype, s); break;
@@ -789,19 +805,27 @@ int msg_gemm(const uint8_t* packed, const uint8_t* wrep, int64_t m, int64_t k, i
   }
   if (e) return e;
   if (flags & MSG_FLAG_LUT_PHASE_ONLY) return MSG_OK;
-  TailVals tv;
-  for (int c = 0; c < 16; ++c) tv.v[c] = (float)values[c];
-  const int64_t total = m * b;
   const uint16_t* tailp =
       p.L.tail ? reinterpret_cast<const uint16_t*>(wrep + p.L.tail_off) : nullptr;
+  return launch_finish(P.partial, p.S, m, b, k, d, tailp, tv, x, x_dtype, scale_mode, q, q_dtype,
+                       y, y_dtype, s);
+}
+
+}  // extern "C"
+
+namespace msg {
+int launch_finish(const float* partial, int S, int64_t m, int64_t b, int64_t k, int d,
+                  const uint16_t* tailp, const TailVals& tv, const void* x, int x_dtype,
+                  int scale_mode, const void* q, int q_dtype, void* y, int y_dtype,
+                  cudaStream_t s) {
+  const int64_t total = m * b;
   // lanes per output: enough threads to cover the SMs, never more than slices
   int lpo = 1;
-  while (lpo < 32 && lpo < p.S && total * lpo < (int64_t)sm_count() * 1024) lpo *= 2;
+  while (lpo < 32 && lpo < S && total * lpo < (int64_t)sm_count() * 1024) lpo *= 2;
   const int grid =
       (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total * lpo, 256), (int64_t)sm_count() * 8));
-  const float* corr = p.sym ? P.corr : nullptr;
 #define MSG_FIN(L)                                                                            \
-  fused_finish_kernel<L><<<grid, 256, 0, s>>>(P.partial, corr, p.S, m, b, k, d, tailp, tv, x, \
+  fused_finish_kernel<L><<<grid, 256, 0, s>>>(partial, S, m, b, k, d, tailp, tv, x,       \
                                               x_dtype, scale_mode, q, q_dtype, y, y_dtype)
   switch (lpo) {
     case 1: MSG_FIN(1); break;
@@ -816,4 +840,5 @@ int msg_gemm(const uint8_t* packed, const uint8_t* wrep, int64_t m, int64_t k, i
   return MSG_OK;
 }
 
-}  // extern "C"
+}  // namespace msg
+

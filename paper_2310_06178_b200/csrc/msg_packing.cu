@@ -14,6 +14,10 @@
 namespace msg {
 
 static thread_local std::string g_last_error;
+static TraceRec* g_trace = nullptr;  // diagnostics: per-CTA trace records
+static bool g_trace_on = false;
+
+TraceRec* trace_buffer() { return g_trace_on ? g_trace : nullptr; }
 
 void set_error(const std::string& s) { g_last_error = s; }
 
@@ -166,6 +170,23 @@ const char* msg_last_error(void) { return g_last_error.c_str(); }
 int msg_version(void) { return 100; }
 
 int msg_device_sm_count(void) { return sm_count(); }
+
+int msg_set_tracing(int on) {
+  g_trace_on = on != 0;
+  if (g_trace_on && !g_trace) {
+    MSG_CUDA_CHECK(cudaMalloc(&g_trace, sizeof(TraceRec) * kTraceMax));  // diagnostics only
+  }
+  if (g_trace_on) MSG_CUDA_CHECK(cudaMemset(g_trace, 0, sizeof(TraceRec) * kTraceMax));
+  return MSG_OK;
+}
+
+int msg_read_trace(uint64_t* host, int max_records) {
+  if (!g_trace) return 0;
+  int n = max_records < kTraceMax ? max_records : kTraceMax;
+  MSG_CUDA_CHECK(cudaDeviceSynchronize());
+  MSG_CUDA_CHECK(cudaMemcpy(host, g_trace, sizeof(TraceRec) * n, cudaMemcpyDeviceToHost));
+  return n;
+}
 
 int msg_pack_codes(const uint8_t* codes, int64_t m, int64_t k, int width, uint8_t* packed,
                    void* stream) {
