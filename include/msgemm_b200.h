@@ -142,12 +142,18 @@ MSG_API int msg_gemm(const uint8_t* packed, const uint8_t* wrep, int64_t m, int6
              int flags, void* stream);
 
 /* ---------- K4: dequantise-then-MMA comparison kernel (gemm.py:206-216 naive_gemm) ---------- */
+/* bytes of the tensor-core tile layout of W ([m/128][k/64][128][32 B], nibbles
+ * permuted for the fp16 magic-number dequantisation) */
+MSG_API int64_t msg_mma_layout_bytes(int64_t m, int64_t k);
+/* int4 / uint4 codebooks only (NOT_SUPPORTED otherwise) */
+MSG_API int msg_repack_mma(const uint8_t* packed, int64_t m, int64_t k, const double* values,
+                           uint8_t* out, void* stream);
 MSG_API int64_t msg_dequant_mma_workspace_bytes(int64_t m, int64_t k, int64_t b);
-/* int4 (width 4, any codebook whose values are exact in fp16) x fp16 X (k,b) -> fp32 Y (m,b),
- * tcgen05.mma kind::f16 with fp32 accumulation in TMEM. */
-MSG_API int msg_dequant_mma(const uint8_t* packed, int64_t m, int64_t k, const double* values,
-                    const void* x_f16, int64_t b, float* y, void* workspace,
-                    int64_t workspace_bytes, void* stream);
+/* Y (m,b) = dequant(W) @ X, X fp16 (k,b), 1 <= b <= 256; tcgen05.mma kind::f16
+ * with fp32 accumulation in TMEM; Y of y_dtype (fp32 or fp16). */
+MSG_API int msg_dequant_mma(const uint8_t* wmma, int64_t m, int64_t k, const double* values,
+                            const void* x, int x_dtype, int64_t b, void* y, int y_dtype,
+                            void* workspace, int64_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

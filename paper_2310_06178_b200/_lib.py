@@ -31,6 +31,7 @@ EXPORTS = (
     "msg_unpack_codes", "msg_group_indices", "msg_encode_values", "msg_lut_build",
     "msg_repacked_bytes", "msg_repack", "msg_gemm_plan", "msg_gemm",
     "msg_dequant_mma_workspace_bytes", "msg_dequant_mma", "msg_set_tracing", "msg_read_trace",
+    "msg_mma_layout_bytes", "msg_repack_mma",
 )
 
 _c_i64 = ctypes.c_int64
@@ -53,8 +54,10 @@ _SIGS = {
     "msg_gemm": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_int, _vp, _vp, _c_int, _c_i64, _c_int,
                           _c_int, _c_i64, _vp, _c_int, _vp, _c_int, _vp, _c_i64, _c_int, _vp]),
     "msg_dequant_mma_workspace_bytes": (_c_i64, [_c_i64, _c_i64, _c_i64]),
-    "msg_dequant_mma": (_c_int, [_vp, _c_i64, _c_i64, _vp, _vp, _c_i64, _vp, _vp, _c_i64,
-                                 _vp]),
+    "msg_dequant_mma": (_c_int, [_vp, _c_i64, _c_i64, _vp, _vp, _c_int, _c_i64, _vp, _c_int,
+                                 _vp, _c_i64, _vp]),
+    "msg_mma_layout_bytes": (_c_i64, [_c_i64, _c_i64]),
+    "msg_repack_mma": (_c_int, [_vp, _c_i64, _c_i64, _vp, _vp, _vp]),
     "msg_set_tracing": (_c_int, [_c_int]),
     "msg_read_trace": (_c_int, [_vp, _c_int]),
 }

@@ -840,5 +840,11 @@ int launch_finish(const float* partial, int S, int64_t m, int64_t b, int64_t k, 
   return MSG_OK;
 }
 
-}  // namespace msg
+int launch_finish_plain(const float* partial, int S, int64_t m, int64_t b, void* y, int y_dtype,
+                        cudaStream_t s) {
+  TailVals tv{};
+  return launch_finish(partial, S, m, b, 0, 1, nullptr, tv, nullptr, MSG_F32, MSG_SCALE_NONE,
+                       nullptr, MSG_F32, y, y_dtype, s);
+}
 
+}  // namespace msg

@@ -1,17 +1,380 @@
-// K4 placeholder: dequantise-then-tcgen05.mma comparison kernel (see msg_mma_tc.cu when built).
+// K4: dequantise-then-tcgen05.mma comparison kernel.
+//
+// The dense baseline the paper argues msGeMM against:
+// Y = dequant(W) @ X with W int4 and X fp16, on the 5th-generation tensor
+// cores.  Spec: naive_gemm(dense(pwm), X) (gemm.py:206-216,
+// packing.py:191-198); the int4 -> fp16 dequantisation is exact and the
+// tensor core accumulates in fp32.
+//
+// Per CTA: a 128-row tile of W (M = 128), the whole (padded) batch N = b,
+// and a slice of K.  Each 64-wide K step:
+//   * TMA bulk copies bring the repacked 128x64 int4 tile (4 KiB) and the
+//     pre-swizzled fp16 X^T tile (N x 128 B) into a NS-deep smem ring;
+//   * the 128 threads dequantise their row (magic-number fp16 conversion:
+//     8 nibbles -> 4 half2 in 4 LOP3 + 4 HFMA2, K3 pre-permutes the nibbles)
+//     into the canonical K-major SWIZZLE_128B operand layout;
+//   * one thread issues 4 tcgen05.mma.kind::f16 (M128 x N x K16) with the
+//     fp32 accumulator in TMEM and commits to an mbarrier that also releases
+//     the ring slot.
+// The epilogue reads TMEM with tcgen05.ld (one warp per 32 rows) and writes
+// fp32 k-split partials, reduced by the shared deterministic finish kernel.
+#include <algorithm>
+
 #include "msg_common.cuh"
+
+namespace msg {
+
+int launch_finish_plain(const float* partial, int S, int64_t m, int64_t b, void* y, int y_dtype,
+                        cudaStream_t s);
+
+constexpr int kMmaBM = 128, kMmaBK = 64;
+constexpr int kMmaTileA = kMmaBM * kMmaBK / 2;  // 4096 packed bytes
+
+static inline int64_t al256(int64_t v) { return (v + 255) / 256 * 256; }
+
+struct MmaShape {
+  int64_t mt, kt, npad;  // 128-row tiles, 64-wide k tiles, padded batch
+};
+static MmaShape mma_shape(int64_t m, int64_t k, int64_t b) {
+  MmaShape s{};
+  s.mt = (m + kMmaBM - 1) / kMmaBM;
+  s.kt = (k + kMmaBK - 1) / kMmaBK;
+  int64_t n = 16;
+  while (n < b) n *= 2;
+  s.npad = n;
+  return s;
+}
+
+}  // namespace msg
+
+extern "C" int64_t msg_mma_layout_bytes(int64_t m, int64_t k) {
+  msg::MmaShape s = msg::mma_shape(m, k, 1);
+  return s.mt * s.kt * msg::kMmaTileA;
+}
+
+namespace msg {
+
+// repacked W: [mt][kt][128 rows][32 bytes]; within each 32-bit word the 8
+// nibbles of k = 8q..8q+7 sit at positions (0,4,1,5,2,6,3,7) and are XORed
+// with `xmask` (8 for two's-complement int4, so stored u = v + 8; 0 for uint4)
+__global__ void repack_mma_kernel(const uint8_t* __restrict__ packed, int64_t m, int64_t k,
+                                  int rb, int xmask, MmaShape S, uint8_t* __restrict__ out) {
+  const int64_t nwords = S.mt * S.kt * kMmaBM * 8;  // 8 words per row per k tile
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nwords;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int q = (int)(t & 7);
+    const int64_t rt = t >> 3;  // (mt, kt, row)
+    const int r = (int)(rt % kMmaBM);
+    const int64_t tile = rt / kMmaBM;
+    const int64_t kti = tile % S.kt, mti = tile / S.kt;
+    const int64_t i = mti * kMmaBM + r;
+    uint32_t w = 0;
+    const int pos[8] = {0, 4, 1, 5, 2, 6, 3, 7};
+    for (int e = 0; e < 8; ++e) {
+      const int64_t j = kti * kMmaBK + q * 8 + e;
+      uint32_t c = 0;
+      if (i < m && j < k) c = (packed[i * rb + (j >> 1)] >> ((j & 1) * 4)) & 0xF;
+      w |= ((c ^ (uint32_t)xmask) & 0xF) << (4 * pos[e]);
+    }
+    reinterpret_cast<uint32_t*>(out)[t] = w;
+  }
+}
+
+// X (k, b) fp16 row-major -> per k tile the K-major SWIZZLE_128B image of X^T:
+// row n, 16-byte chunk c at (n/8)*1024 + (n%8)*128 + ((c ^ n%8) * 16)
+__global__ void prep_xt_kernel(const __half* __restrict__ x, int64_t k, int64_t b, MmaShape S,
+                               uint8_t* __restrict__ out) {
+  const int64_t tile_bytes = S.npad * 128;
+  const int64_t nchunks = S.kt * S.npad * 8;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nchunks;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(t & 7);
+    const int64_t n = (t >> 3) % S.npad;
+    const int64_t kti = (t >> 3) / S.npad;
+    uint32_t wv[4];
+    for (int e = 0; e < 4; ++e) {
+      __half lo = __float2half(0.f), hi = __float2half(0.f);
+      const int64_t j = kti * kMmaBK + c * 8 + 2 * e;
+      if (n < b && j < k) lo = x[j * b + n];
+      if (n < b && j + 1 < k) hi = x[(j + 1) * b + n];
+      __half2 h2 = __halves2half2(lo, hi);
+      wv[e] = *reinterpret_cast<uint32_t*>(&h2);
+    }
+    const int64_t off = kti * tile_bytes + (n >> 3) * 1024 + (n & 7) * 128 + ((c ^ (n & 7)) * 16);
+    *reinterpret_cast<uint4*>(out + off) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+  }
+}
+
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) |  // start, LBO = 16 B
+         ((uint64_t)(1024 >> 4) << 32) |                            // SBO = 1024 B (8-row group)
+         ((uint64_t)1 << 46) |                                       // descriptor version (sm_100)
+         ((uint64_t)2 << 61);                                        // SWIZZLE_128B
+}
+
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                        uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::
+                   "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+struct MmaParams {
+  const uint8_t* wt;   // repacked W tiles
+  const uint8_t* xt;   // swizzled X^T tiles
+  float* partial;      // [S][m][b]
+  int64_t m, b, kt_total, kt_per_split;
+  float sub_lo, sub_hi;  // dequant constants: v = h - sub (lo lanes), v = h/16 - sub (hi lanes)
+};
+
+template <int N, int NS>
+__global__ void __launch_bounds__(128, 1) dq_mma_kernel(MmaParams P) {
+  constexpr int TB = N * 128;  // B tile bytes
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-align the carve-up (SWIZZLE_128B operands need 1024 B alignment)
+  uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* opA = smem;                              // [2][16 KiB]
+  uint8_t* stB = opA + 2 * 16384;                   // [NS][TB]
+  uint8_t* stA = stB + NS * TB;                     // [NS][4 KiB]
+  uint64_t* full = reinterpret_cast<uint64_t*>(stA + NS * kMmaTileA);  // [NS]
+  uint64_t* done = full + NS;                                           // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 2);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t mt = blockIdx.x, split = blockIdx.y;
+  const int64_t kt0 = split * P.kt_per_split;
+  const int64_t kt1 = std::min<int64_t>(P.kt_total, kt0 + P.kt_per_split);
+  const int nloc = (int)std::max<int64_t>(0, kt1 - kt0);
+  constexpr uint32_t kCols = N < 32 ? 32 : N;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(kCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1);
+    mbar_init(&done[0], 1);
+    mbar_init(&done[1], 1);
+    fence_mbar_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  auto issue = [&](int i) {  // local k tile i -> ring slot i % NS (thread 0)
+    const int slot = i % NS;
+    const int64_t kt = kt0 + i;
+    mbar_expect_tx(&full[slot], kMmaTileA + TB);
+    bulk_g2s(stA + slot * kMmaTileA, P.wt + (mt * P.kt_total + kt) * kMmaTileA, kMmaTileA,
+             &full[slot]);
+    bulk_g2s(stB + slot * TB, P.xt + kt * TB, TB, &full[slot]);
+  };
+  if (tid == 0)
+    for (int i = 0; i < NS && i < nloc; ++i) issue(i);
+
+  // idesc: D f32, A/B f16, both K-major, N, M = 128
+  constexpr uint32_t idesc = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  const __half2 sub_lo = __float2half2_rn(P.sub_lo);
+  const __half2 sub_hi = __float2half2_rn(P.sub_hi);
+  const __half2 sixteenth = __float2half2_rn(1.0f / 16.0f);
+
+  for (int i = 0; i < nloc; ++i) {
+    const int slot = i % NS, buf = i & 1;
+    mbar_wait(&full[slot], (uint32_t)((i / NS) & 1));
+    if (i >= 2) mbar_wait(&done[buf], (uint32_t)(((i - 2) >> 1) & 1));
+    // ---- dequantise row `tid` of the tile into the swizzled A operand
+    {
+      const uint4* src = reinterpret_cast<const uint4*>(stA + slot * kMmaTileA + tid * 32);
+      const uint4 p0 = src[0], p1 = src[1];
+      const uint32_t words[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+      uint8_t* dst_row = opA + buf * 16384 + (tid >> 3) * 1024 + (tid & 7) * 128;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {  // 16-byte chunk c = k 8c..8c+7 = word c
+        uint32_t w = words[c];
+        uint32_t h[4];
+        // nibbles (pos 0,4) = (k0,k1): low lanes; (1,5) = (k2,k3): x16 lanes; then >> 8
+        h[0] = (w & 0x000F000Fu) | 0x64006400u;
+        h[1] = (w & 0x00F000F0u) | 0x64006400u;
+        w >>= 8;
+        h[2] = (w & 0x000F000Fu) | 0x64006400u;
+        h[3] = (w & 0x00F000F0u) | 0x64006400u;
+        __half2 v0 = __hsub2(*reinterpret_cast<__half2*>(&h[0]), sub_lo);
+        __half2 v1 = __hfma2(*reinterpret_cast<__half2*>(&h[1]), sixteenth, sub_hi);
+        __half2 v2 = __hsub2(*reinterpret_cast<__half2*>(&h[2]), sub_lo);
+        __half2 v3 = __hfma2(*reinterpret_cast<__half2*>(&h[3]), sixteenth, sub_hi);
+        uint4 o = make_uint4(*reinterpret_cast<uint32_t*>(&v0), *reinterpret_cast<uint32_t*>(&v1),
+                             *reinterpret_cast<uint32_t*>(&v2), *reinterpret_cast<uint32_t*>(&v3));
+        *reinterpret_cast<uint4*>(dst_row + ((c ^ (tid & 7)) * 16)) = o;
+      }
+    }
+    fence_proxy_async();  // generic smem writes -> visible to the tensor core (async proxy)
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint64_t ad = umma_desc_sw128(smem_u32(opA + buf * 16384));
+      const uint64_t bd = umma_desc_sw128(smem_u32(stB + slot * TB));
+#pragma unroll
+      for (int ks = 0; ks < kMmaBK / 16; ++ks)  // K = 16 per instruction = 32 bytes
+        mma_f16(tmem, ad + 2 * ks, bd + 2 * ks, idesc, (i > 0 || ks > 0) ? 1u : 0u);
+      mma_commit(&done[buf]);
+      // slot of tile i-1 is free once its MMAs are done: refill with tile i-1+NS
+      if (i >= 1 && i - 1 + NS < nloc) {
+        mbar_wait(&done[(i - 1) & 1], (uint32_t)(((i - 1) >> 1) & 1));
+        issue(i - 1 + NS);
+      }
+    }
+  }
+  // ---- epilogue: TMEM -> registers -> fp32 partials
+  const int64_t row = mt * kMmaBM + warp * 32 + lane;
+  float* dst = P.partial + (split * P.m + row) * P.b;
+  if (nloc > 0) {
+    mbar_wait(&done[(nloc - 1) & 1], (uint32_t)(((nloc - 1) >> 1) & 1));
+    tc_fence_after();
+#pragma unroll
+    for (int c0 = 0; c0 < N; c0 += 16) {
+      uint32_t r[16];
+      const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+          "%14,%15}, [%16];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+            "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+            "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (row < P.m) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          if (c0 + e < P.b) dst[c0 + e] = __uint_as_float(r[e]);
+      }
+    }
+  } else if (row < P.m) {
+    for (int64_t e = 0; e < P.b; ++e) dst[e] = 0.f;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols));
+}
+
+template <int N, int NS>
+static int launch_dq(const MmaParams& P, const MmaShape& S, int splits, cudaStream_t s) {
+  const int smem = 1024 + 2 * 16384 + NS * (N * 128 + kMmaTileA) + (NS + 2) * 8 + 16;
+  static int configured_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured_dev != dev) {
+    MSG_CUDA_CHECK(cudaFuncSetAttribute(dq_mma_kernel<N, NS>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured_dev = dev;
+  }
+  dim3 grid((unsigned)S.mt, (unsigned)splits);
+  dq_mma_kernel<N, NS><<<grid, 128, smem, s>>>(P);
+  MSG_LAUNCH_CHECK();
+  return MSG_OK;
+}
+
+static int mma_splits(const MmaShape& S) {
+  int64_t sp = std::max<int64_t>(1, (int64_t)sm_count() / std::max<int64_t>(1, S.mt));
+  return (int)std::min<int64_t>(sp, std::max<int64_t>(1, S.kt / 4));
+}
+
+}  // namespace msg
 
 using namespace msg;
 
 extern "C" int64_t msg_dequant_mma_workspace_bytes(int64_t m, int64_t k, int64_t b) {
-  (void)m; (void)k; (void)b;
-  return 0;
+  MmaShape S = mma_shape(m, k, b);
+  const int sp = mma_splits(S);
+  return al256(S.kt * S.npad * 128) + al256((int64_t)sp * m * b * 4);
 }
 
-extern "C" int msg_dequant_mma(const uint8_t* packed, int64_t m, int64_t k, const double* values,
-                               const void* x_f16, int64_t b, float* y, void* workspace,
-                               int64_t workspace_bytes, void* stream) {
-  (void)packed; (void)m; (void)k; (void)values; (void)x_f16; (void)b; (void)y;
-  (void)workspace; (void)workspace_bytes; (void)stream;
-  return fail(MSG_ERR_UNSUPPORTED, "dequant-MMA comparison kernel not built yet");
+extern "C" int msg_dequant_mma(const uint8_t* wmma, int64_t m, int64_t k, const double* values,
+                               const void* x, int x_dtype, int64_t b, void* y, int y_dtype,
+                               void* workspace, int64_t ws_bytes, void* stream) {
+  if (x_dtype != MSG_F16)
+    return fail(MSG_ERR_UNSUPPORTED, "the dequant-MMA comparison kernel takes fp16 activations");
+  if (b < 1 || b > 256)
+    return fail(MSG_ERR_UNSUPPORTED, "dequant-MMA supports 1 <= b <= 256 (got %lld)", (long long)b);
+  // int4 (two's complement) or uint4 alphabets: v = u - off with u the stored nibble
+  double off;
+  bool int4 = true, uint4 = true;
+  for (int c = 0; c < 16; ++c) {
+    int4 = int4 && values[c] == (double)(c < 8 ? c : c - 16);
+    uint4 = uint4 && values[c] == (double)c;
+  }
+  if (int4) off = 8.0;
+  else if (uint4) off = 0.0;
+  else return fail(MSG_ERR_UNSUPPORTED, "dequant-MMA supports the int4/uint4 codebooks");
+  if (ws_bytes < msg_dequant_mma_workspace_bytes(m, k, b))
+    return fail(MSG_ERR_WORKSPACE, "workspace too small for dequant-MMA");
+  if (m == 0) return MSG_OK;
+  cudaStream_t s = as_stream(stream);
+  MmaShape S = mma_shape(m, k, b);
+  const int splits = mma_splits(S);
+  uint8_t* xt = reinterpret_cast<uint8_t*>(workspace);
+  float* partial = reinterpret_cast<float*>((char*)workspace + al256(S.kt * S.npad * 128));
+  {
+    const int64_t n = S.kt * S.npad * 8;
+    const int grid = (int)std::min<int64_t>(ceil_div(n, 256), (int64_t)sm_count() * 8);
+    prep_xt_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const __half*>(x), k, b, S, xt);
+    MSG_LAUNCH_CHECK();
+  }
+  MmaParams P{};
+  P.wt = wmma;
+  P.xt = xt;
+  P.partial = partial;
+  P.m = m;
+  P.b = b;
+  P.kt_total = S.kt;
+  P.kt_per_split = ceil_div(S.kt, splits);
+  // magic-number dequant: (1024 + u) - (1024 + off); (1024*16 + 16u)/16 - (1024 + off)
+  P.sub_lo = (float)(1024.0 + off);
+  P.sub_hi = (float)(-(64.0 + off));
+  int e;
+  switch (S.npad) {
+    case 16: e = launch_dq<16, 8>(P, S, splits, s); break;
+    case 32: e = launch_dq<32, 8>(P, S, splits, s); break;
+    case 64: e = launch_dq<64, 6>(P, S, splits, s); break;
+    case 128: e = launch_dq<128, 5>(P, S, splits, s); break;
+    default: e = launch_dq<256, 4>(P, S, splits, s); break;
+  }
+  if (e) return e;
+  return launch_finish_plain(partial, splits, m, b, y, y_dtype, s);
+}
+
+extern "C" int msg_repack_mma(const uint8_t* packed, int64_t m, int64_t k,
+                              const double* values, uint8_t* out, void* stream) {
+  bool int4 = true, uint4 = true;
+  for (int c = 0; c < 16; ++c) {
+    int4 = int4 && values[c] == (double)(c < 8 ? c : c - 16);
+    uint4 = uint4 && values[c] == (double)c;
+  }
+  if (!int4 && !uint4)
+    return fail(MSG_ERR_UNSUPPORTED, "dequant-MMA supports the int4/uint4 codebooks");
+  const int xmask = int4 ? 8 : 0;
+  cudaStream_t s = as_stream(stream);
+  MmaShape S = mma_shape(m, k, 1);
+  const int64_t n = S.mt * S.kt * kMmaBM * 8;
+  if (n == 0) return MSG_OK;
+  const int grid = (int)std::min<int64_t>(ceil_div(n, 256), (int64_t)sm_count() * 16);
+  repack_mma_kernel<<<grid, 256, 0, s>>>(packed, m, k, row_bytes(k, 4), xmask, S, out);
+  MSG_LAUNCH_CHECK();
+  return MSG_OK;
 }

@@ -25,7 +25,7 @@ from .lut import DEFAULT_BUDGET, block_nbytes, build_lut
 from .packing import PackedWeightMatrix, PerGroup, PerRow, group_indices
 
 __all__ = ["OpCount", "msgemm", "msgemm_counted", "msgemm_traced", "naive_gemm",
-           "naive_gemm_counted"]
+           "naive_gemm_counted", "dequant_gemm"]
 
 
 @dataclass(frozen=True)
@@ -254,3 +254,35 @@ def naive_gemm_counted(W, X):
     m, k = (int(s) for s in Wa.shape)
     b = int(Xm.shape[1])
     return Y, OpCount(fma=m * k * b, mem_weights=m * k, mem_activations=k * b)
+
+
+def dequant_gemm(pwm: PackedWeightMatrix, X, out_dtype=np.float32, out=None):
+    """Dense comparison baseline: dequantise int4 W to fp16 and multiply on the
+    tcgen05 tensor cores (K4, csrc/msg_mma.cu); fp32 accumulation in TMEM.
+
+    X must be fp16 (k,) or (k, b) with b <= 256; int4/uint4 codebooks, no
+    scales.  Same result contract as naive_gemm(dense(pwm), X) (gemm.py:206-216).
+    """
+    pwm = _ensure_device_pwm(pwm)
+    if pwm.scales is not None:
+        raise NotImplementedError("dequant_gemm does not apply scales")
+    Xm, was_vector = _as_matrix(X)
+    if int(Xm.shape[0]) != pwm.k:
+        raise ValueError(f"activation rows {Xm.shape[0]} != weight columns {pwm.k}")
+    dev = _lib.require_device()
+    t = _lib.torch()
+    lib = _lib.lib()
+    m, k, b = pwm.m, pwm.k, int(Xm.shape[1])
+    xd = _lib.to_device(Xm, dev)
+    y_dt = _lib.torch_dtype_of(np.dtype(out_dtype))
+    Y = out if out is not None else t.empty((m, b), dtype=y_dt, device=dev)
+    if m and b:
+        wt = pwm.device_mma_layout(dev)
+        ws = _lib.workspace(lib.msg_dequant_mma_workspace_bytes(m, k, b), dev)
+        _lib.check(lib.msg_dequant_mma(
+            _lib.ptr(wt), m, k, _lib.host_doubles(pwm.codebook.values), _lib.ptr(xd),
+            _lib.dtype_code(xd.dtype), b, _lib.ptr(Y), _lib.dtype_code(y_dt), _lib.ptr(ws),
+            ws.numel(), _lib.stream_ptr()))
+    if was_vector:
+        Y = Y.reshape(m, b)[:, 0]
+    return Y if _lib.is_torch(X) and X.is_cuda else Y.cpu().numpy()

@@ -99,6 +99,20 @@ class PackedWeightMatrix:
             cache[key] = out
         return cache[key]
 
+    def device_mma_layout(self, dev):
+        """The tensor-core tile layout of W (K4 comparison kernel), built once."""
+        cache = self._device_cache
+        key = ("mma", dev.index)
+        if key not in cache:
+            t = _lib.torch()
+            nbytes = _lib.lib().msg_mma_layout_bytes(self.m, self.k)
+            out = t.empty(max(int(nbytes), 1), dtype=t.uint8, device=dev)
+            _lib.check(_lib.lib().msg_repack_mma(
+                _lib.ptr(self.device_data(dev)), self.m, self.k,
+                _lib.host_doubles(self.codebook.values), _lib.ptr(out), _lib.stream_ptr()))
+            cache[key] = out
+        return cache[key]
+
     def device_scales(self, dev):
         cache = self._device_cache
         key = ("q", dev.index)

@@ -53,7 +53,11 @@ def _plan(m, k, b, d, dt=_lib.F16, flags=0, cb=None, scale=0, gs=0):
                                      (65536, 8192, 8, 3)])
 def test_plan_configs_take_fused_symmetric_path(m, k, b, d):
     st, lay, sym, ws = _plan(m, k, b, d)
-    assert st == 0 and lay == _lib.LAYOUT_QUAD and sym == 1 and ws > 0
+    want = _lib.LAYOUT_LANE if (b == 1 and d == 3) else _lib.LAYOUT_QUAD
+    assert st == 0 and lay == want and sym == 1 and ws > 0
+    # the row-block kernel remains selectable for the GEMV shapes
+    st, lay, sym, ws = _plan(m, k, b, d, flags=_lib.FLAG_NO_LANE)
+    assert st == 0 and lay == _lib.LAYOUT_QUAD
 
 
 def test_plan_routes_to_generic():
@@ -77,6 +81,8 @@ def test_plan_errors_map_like_reference():
 
 def test_repacked_bytes():
     lib = _lib.load_library()
+    assert lib.msg_repacked_bytes(4096, 4096, 3, _lib.LAYOUT_LANE) >= 4096 * 4096 // 2
+    assert lib.msg_mma_layout_bytes(8192, 8192) == 8192 * 8192 // 2
     assert lib.msg_repacked_bytes(65536, 8192, 3, _lib.LAYOUT_QUAD) >= 65536 * 8192 // 2
     assert lib.msg_repacked_bytes(10, 10, 4, _lib.LAYOUT_QUAD) == -1
     assert lib.msg_repacked_bytes(10, 10, 2, _lib.LAYOUT_NONE) == 0

@@ -114,3 +114,35 @@ def test_properties(name):
     for c in (0, cfg.b - 1):
         yc = mg.msgemm(pwm, xd[:, c].contiguous(), cfg.d)
         assert orc.rel_error(yc[:256].cpu().numpy(), W, X[:, c]) <= 2e-3
+
+
+@pytest.mark.parametrize("m,k,b", [(128, 64, 1), (300, 200, 3), (1024, 1024, 16), (8192, 8192, 1),
+                                   (8192, 8192, 16), (8192, 8192, 64), (8192, 8192, 256),
+                                   (11008, 4096, 16), (4096, 4096, 1)])
+def test_dequant_mma_matches_dense(m, k, b):
+    """K4 (tcgen05 kind::f16, fp32 TMEM accumulation) against the exact dense
+    product: bit-exact for integer-valued X (partials < 2^24), 2e-3 rule for
+    N(0,1) fp16 X."""
+    rng = np.random.default_rng(m + k + b)
+    data = rng.integers(0, 256, size=(m, (k + 1) // 2), dtype=np.uint8)
+    pwm = mg.PackedWeightMatrix(m=m, k=k, width=4, data=data, codebook=mg.int4_codebook())
+    W = orc.dense(data, k, 4, INT4)
+    Xi = rng.integers(-127, 128, size=(k, b))
+    yi = mg.dequant_gemm(pwm, Xi.astype(np.float16))
+    assert yi.dtype == np.float32 and yi.shape == (m, b)
+    assert np.array_equal(yi.astype(np.int64), W.astype(np.int64) @ Xi)
+    X = rng.standard_normal((k, b)).astype(np.float16)
+    y = mg.dequant_gemm(pwm, X)
+    assert orc.rel_error(y, W, X) <= 2e-3
+    y16 = mg.dequant_gemm(pwm, torch.from_numpy(X).cuda(), out_dtype=np.float16)
+    assert y16.dtype == torch.float16
+
+
+def test_dequant_mma_uint4_and_vector():
+    rng = np.random.default_rng(9)
+    codes = rng.integers(0, 16, size=(200, 96))
+    pwm = mg.from_codes(codes, mg.uint4_codebook())
+    x = rng.integers(-50, 50, size=96).astype(np.float16)
+    y = mg.dequant_gemm(pwm, x)
+    assert y.shape == (200,)
+    assert np.array_equal(y.astype(np.int64), codes.astype(np.int64) @ x.astype(np.int64))
