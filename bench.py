@@ -237,8 +237,14 @@ def main():
                                           codebook=mg.int4_codebook()))
     Yshard = torch.empty((mr, cfg.b), dtype=y_dt, device=dev)
     Yfull = torch.empty((cfg.m, cfg.b), dtype=y_dt, device=dev) if world > 1 else Yshard
+    TC = -1  # pseudo-flag: the dequant + tcgen05.mma comparison kernel (K4) instead of msGeMM
+    xd16 = xd.half()
+    Ytc = torch.empty((mr, cfg.b), dtype=torch.float32, device=dev)
 
     def step(i, flags=0):
+        if flags == TC:
+            mg.dequant_gemm(pwms[i % ncopies], xd16, out=Ytc)
+            return
         mg.msgemm(pwms[i % ncopies], xd, cfg.d, out=Yshard, _flags=flags, **kw)
         if world > 1 and not flags:
             dist.all_gather_into_tensor(Yfull, Yshard)
@@ -306,6 +312,13 @@ def main():
         step(i, _lib.FLAG_LUT_PHASE_ONLY)
     timed(min(args.steps, 16), _lib.FLAG_LUT_PHASE_ONLY)
     ms_lut = timed(args.steps, _lib.FLAG_LUT_PHASE_ONLY)
+    # the dense tensor-core baseline on the same shard (context, not the metric)
+    ms_tc = None
+    if cfg.b <= 256:
+        for i in range(max(3, ncopies)):
+            step(i, TC)
+        timed(min(args.steps, 16), TC)
+        ms_tc = timed(args.steps, TC)
 
     # end to end through the public API: pinned host X in, host Y out, every step
     e2e_steps = args.e2e_steps or max(3, min(args.steps, 50))
@@ -374,6 +387,11 @@ def main():
                 "d2h_bytes_per_step": cfg.m * cfg.b * y_item,
                 "path": "msgemm(pwm, pinned host X) -> host Y" if world == 1 else
                         "H2D X, msgemm shard, NCCL all-gather, D2H Y"},
+        "tensor_core_baseline": None if ms_tc is None else {
+            "kernel": "K4: int4->fp16 dequant + tcgen05.mma kind::f16, fp32 TMEM accumulation",
+            "ms_per_step": ms_tc, "value": effective_ops(shard_cfg) / (ms_tc * 1e-3) / 1e9,
+            "unit": "GOP/s (this rank's shard, no all-gather)",
+            "hbm_frac": algorithmic_bytes(shard_cfg, 2, 4) / (ms_tc * 1e-3) / 1e9 / peaks["hbm_gbs"]},
         "gpu_launches": 2 * args.steps,
         "clocks": clocks,
     }

@@ -196,7 +196,7 @@ def workspace(nbytes: int, dev):
     key = (dev.index, t.cuda.current_stream(dev).cuda_stream)
     buf = _ws.get(key)
     if buf is None or buf.numel() < nbytes:
-        buf = t.empty(max(int(nbytes), 256), dtype=t.uint8, device=dev)
+        buf = t.zeros(max(int(nbytes), 256), dtype=t.uint8, device=dev)
         _ws[key] = buf
     return buf
 

@@ -518,34 +518,38 @@ struct TailVals {
   float v[16];
 };
 
-// LPO lanes cooperate on one output: lane j sums slices j, j+LPO, ... in order,
-// then a fixed butterfly combines them -- deterministic run to run.
-template <int LPO>
-__global__ void fused_finish_kernel(const float* __restrict__ partial,
-                                    int S, int64_t m, int64_t b,
-                                    int64_t k, int d, const uint16_t* __restrict__ tailp,
-                                    TailVals vals, const void* x, int x_dtype,
-                                    int scale_mode, const void* q, int q_dtype, void* y,
-                                    int y_dtype) {
+// A 256-thread block reduces 256/SG consecutive outputs: slice group g (of SG)
+// sums slices g, g+SG, ... in order for each output (lanes = consecutive
+// outputs, so every load is a coalesced 128-byte row), then the SG partial
+// sums are combined in fixed order -- deterministic run to run.
+template <int SG>
+__global__ void __launch_bounds__(256) fused_finish_kernel(
+    const float* __restrict__ partial, int S, int64_t m, int64_t b, int64_t k, int d,
+    const uint16_t* __restrict__ tailp, TailVals vals, const void* x, int x_dtype, int scale_mode,
+    const void* q, int q_dtype, void* y, int y_dtype) {
+  constexpr int OPB = 256 / SG;  // outputs per block
+  __shared__ float red[SG][OPB];
   const int64_t nb = k / d;
   const int tail = (int)(k - nb * d);
   const int64_t total = m * b;
-  const int lane = threadIdx.x % LPO;
-  const int64_t per_block = blockDim.x / LPO;
-  for (int64_t t0 = (int64_t)blockIdx.x * per_block; t0 < total;
-       t0 += (int64_t)gridDim.x * per_block) {
-    const int64_t t = t0 + threadIdx.x / LPO;
+  const int og = threadIdx.x % OPB, sg = threadIdx.x / OPB;
+  for (int64_t t0 = (int64_t)blockIdx.x * OPB; t0 < total; t0 += (int64_t)gridDim.x * OPB) {
+    const int64_t t = t0 + og;
     float s = 0.f;
     if (t < total) {
-      int sl = lane;
-#pragma unroll 4
-      for (; sl < S; sl += LPO) s += partial[(int64_t)sl * total + t];
+#pragma unroll 8
+      for (int sl = sg; sl < S; sl += SG) s += __ldcg(partial + (int64_t)sl * total + t);
     }
-    if constexpr (LPO > 1) {
+    if constexpr (SG > 1) {
+      red[sg][og] = s;
+      __syncthreads();
+      if (sg == 0) {
 #pragma unroll
-      for (int o = LPO / 2; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, LPO);
+        for (int g = 1; g < SG; ++g) s += red[g][og];
+      }
+      __syncthreads();
     }
-    if (t < total && lane == 0) {
+    if (t < total && sg == 0) {
       const int64_t i = t / b, c = t - i * b;
       if (tail) {
         uint32_t tc = tailp[i];
@@ -819,21 +823,20 @@ int launch_finish(const float* partial, int S, int64_t m, int64_t b, int64_t k, 
                   int scale_mode, const void* q, int q_dtype, void* y, int y_dtype,
                   cudaStream_t s) {
   const int64_t total = m * b;
-  // lanes per output: enough threads to cover the SMs, never more than slices
-  int lpo = 1;
-  while (lpo < 32 && lpo < S && total * lpo < (int64_t)sm_count() * 1024) lpo *= 2;
+  // slice groups per output: enough loads in flight to cover the SMs
+  int sg = 1;
+  while (sg < 8 && 2 * sg <= S && total * sg < (int64_t)sm_count() * 2048) sg *= 2;
+  const int opb = 256 / sg;
   const int grid =
-      (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total * lpo, 256), (int64_t)sm_count() * 8));
-#define MSG_FIN(L)                                                                            \
-  fused_finish_kernel<L><<<grid, 256, 0, s>>>(partial, S, m, b, k, d, tailp, tv, x,       \
-                                              x_dtype, scale_mode, q, q_dtype, y, y_dtype)
-  switch (lpo) {
+      (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, opb), (int64_t)sm_count() * 16));
+#define MSG_FIN(G)                                                                            \
+  fused_finish_kernel<G><<<grid, 256, 0, s>>>(partial, S, m, b, k, d, tailp, tv, x, x_dtype,  \
+                                              scale_mode, q, q_dtype, y, y_dtype)
+  switch (sg) {
     case 1: MSG_FIN(1); break;
     case 2: MSG_FIN(2); break;
     case 4: MSG_FIN(4); break;
-    case 8: MSG_FIN(8); break;
-    case 16: MSG_FIN(16); break;
-    default: MSG_FIN(32); break;
+    default: MSG_FIN(8); break;
   }
 #undef MSG_FIN
   MSG_LAUNCH_CHECK();
