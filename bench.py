@@ -35,6 +35,7 @@ sys.path.insert(0, str(ROOT))
 from paper_2310_06178_b200.workloads import CONFIGS, algorithmic_bytes, effective_ops  # noqa: E402
 
 L2_BYTES = 126 * 1024 * 1024
+EXTRA_FLAGS = int(os.environ.get("MSG_BENCH_FLAGS", "0"))  # experiments only (C-ABI flag bits)
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
 
@@ -245,7 +246,7 @@ def main():
         if flags == TC:
             mg.dequant_gemm(pwms[i % ncopies], xd16, out=Ytc)
             return
-        mg.msgemm(pwms[i % ncopies], xd, cfg.d, out=Yshard, _flags=flags, **kw)
+        mg.msgemm(pwms[i % ncopies], xd, cfg.d, out=Yshard, _flags=flags | EXTRA_FLAGS, **kw)
         if world > 1 and not flags:
             dist.all_gather_into_tensor(Yfull, Yshard)
 

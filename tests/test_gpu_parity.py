@@ -100,7 +100,7 @@ def _run_flags(pwm, X, d, flags):
     Y = torch.empty((m, b), dtype=xd.dtype, device=dev)
     q = pwm.device_scales(dev)
     wrep = pwm.device_layout(dev, d, lay.value, sym.value) if lay.value else None
-    wsb = torch.empty(max(ws.value, 256), dtype=torch.uint8, device=dev)
+    wsb = torch.zeros(max(ws.value, 256), dtype=torch.uint8, device=dev)
     _lib.check(lib.msg_gemm(_lib.ptr(pwm.device_data(dev)), _lib.ptr(wrep), m, k, pwm.width,
                             vals, _lib.ptr(xd), code, b, d, mode, gs, _lib.ptr(q),
                             _lib.dtype_code(q.dtype) if q is not None else 0, _lib.ptr(Y), code,
