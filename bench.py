@@ -143,12 +143,17 @@ class CpuArm:
                 f"{seconds:.2f}s total")
 
 
-def cpu_baseline(cfg, target_s: float = 10.0):
+def cpu_baseline(cfg, target_s: float = 12.0):
+    """Row chunks of ~1 s each until target_s of CPU work has been timed."""
     arm = CpuArm(cfg)
-    rows = arm.rows_for(target_s)
-    t = arm.run(0, rows)
-    return {"value": arm.gops(rows, t), "unit": "GOP/s", "cores": arm.cores, "kind": "port",
-            "sample": arm.describe(rows, t)}
+    rows = arm.rows_for(1.0)
+    total_t, total_rows, n = 0.0, 0, 0
+    while total_t < target_s:
+        total_t += arm.run(total_rows, rows)
+        total_rows += rows
+        n += 1
+    return {"value": arm.gops(total_rows, total_t), "unit": "GOP/s", "cores": arm.cores,
+            "kind": "port", "sample": arm.describe(rows, total_t, n)}
 
 
 def run_reference(args, rank, world):
@@ -242,12 +247,12 @@ def main():
     xd16 = xd.half()
     Ytc = torch.empty((mr, cfg.b), dtype=torch.float32, device=dev)
 
-    def step(i, flags=0):
+    def step(i, flags=0, gather=True):
         if flags == TC:
             mg.dequant_gemm(pwms[i % ncopies], xd16, out=Ytc)
             return
         mg.msgemm(pwms[i % ncopies], xd, cfg.d, out=Yshard, _flags=flags | EXTRA_FLAGS, **kw)
-        if world > 1 and not flags:
+        if world > 1 and not flags and gather:
             dist.all_gather_into_tensor(Yfull, Yshard)
 
     def barrier():
@@ -257,37 +262,48 @@ def main():
     use_graphs = os.environ.get("MSG_BENCH_NO_GRAPH", "0") != "1"
     graphs = {}
 
-    def graph_for(n, flags):
-        """One CUDA graph holding n consecutive steps (weight copies 0..n-1 mod ncopies):
-        kernel launches are replayed without host overhead."""
-        key = (n, flags)
+    def graph_for(n, flags, start=0):
+        """One CUDA graph holding the kernels of n consecutive steps (weight copies
+        start..start+n-1 mod ncopies): launches replay without host overhead.
+        Collectives are never captured; with N > 1 ranks each step replays a
+        one-step graph and then all-gathers eagerly."""
+        key = (n, flags, start)
         if key not in graphs:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
-                for i in range(n):
-                    step(i, flags)
+                for i in range(start, start + n):
+                    step(i, flags, gather=False)
             graphs[key] = g
         return graphs[key]
 
     def timed(nsteps, flags=0):
-        per = ncopies * max(1, math.ceil(8 / ncopies))
-        reps, rem = divmod(nsteps, per)
-        if use_graphs:
-            g_full = graph_for(per, flags) if reps else None
-            g_rem = graph_for(rem, flags) if rem else None
         barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        if use_graphs:
+        if use_graphs and world == 1:
+            per = ncopies * max(1, math.ceil(8 / ncopies))
+            reps, rem = divmod(nsteps, per)
+            g_full = graph_for(per, flags) if reps else None
+            g_rem = graph_for(rem, flags) if rem else None
+            e0.record()
             for _ in range(reps):
                 g_full.replay()
             if rem:
                 g_rem.replay()
+            e1.record()
+        elif use_graphs:
+            gs = [graph_for(1, flags, c) for c in range(ncopies)]
+            e0.record()
+            for i in range(nsteps):
+                gs[i % ncopies].replay()
+                if flags == 0:
+                    dist.all_gather_into_tensor(Yfull, Yshard)
+            e1.record()
         else:
+            e0.record()
             for i in range(nsteps):
                 step(i, flags)
-        e1.record()
+            e1.record()
         torch.cuda.synchronize()
         barrier()
         ms = e0.elapsed_time(e1)

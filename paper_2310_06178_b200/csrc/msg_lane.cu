@@ -107,6 +107,12 @@ __device__ __forceinline__ void fhfma_l(float& acc, unsigned short h, unsigned s
   asm("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(acc) : "h"(h), "h"(s16));
 }
 
+__device__ __forceinline__ uint32_t mul_hi_u32(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+
 template <int N>
 __device__ __forceinline__ uint32_t funnel_r(uint32_t lo, uint32_t hi) {
   uint32_t r;
@@ -140,32 +146,57 @@ template <> __device__ __forceinline__ float ldx_l<__half>(const void* p, int64_
 // (T ^ lane) * 4 at bits 2..6; the fp16 entry is accumulated with FHFMA.
 template <int T>
 __device__ __forceinline__ void lookup(const uint32_t (&w)[12], uint32_t xt, uint32_t S,
-                                       uint32_t tab, float& acc) {
-  constexpr int B = 10 * T - 7;  // stream bit that lands at bit 0 of d
+                                       float& acc) {
+  // The row field occupies stream bits [10T, 10T+10) and must land at bits
+  // 7..16.  Shifts that stay inside one word use the FMA pipe (IMAD.SHL /
+  // IMAD.HI as >>) so the ALU pipe -- the bound of this kernel -- only does the
+  // masking and the final 3-input add.
+  constexpr int S0 = (10 * T) & 31, K = (10 * T) >> 5;
   uint32_t d;
-  if constexpr (T == 0) d = w[0] << 7;
-  else d = funnel_r<(B & 31)>(w[B >> 5], w[(B >> 5) + 1]);
+  if constexpr (S0 + 10 <= 32) {
+    if constexpr (S0 == 7) d = w[K];
+    else if constexpr (S0 < 7) d = w[K] << (7 - S0);
+    else d = mul_hi_u32(w[K], 1u << (39 - S0));  // == w[K] >> (S0 - 7)
+  } else {
+    constexpr int B = 10 * T - 7;
+    d = funnel_r<(B & 31)>(w[B >> 5], w[(B >> 5) + 1]);
+  }
   uint32_t hb;  // half-select bit T of w[11] moved to bit 1
   if constexpr (T == 0) hb = w[11] << 1;
-  else hb = w[11] >> (T - 1);
-  const uint32_t off = ((d & 0x1FF80u) | xt) | (hb & 2u);
-  unsigned short h;
-  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(tab + off));
-  unsigned short s0, s1;
-  asm("mov.b32 {%0, %1}, %2;" : "=h"(s0), "=h"(s1) : "r"(S));
-  fhfma_l(acc, h, (T & 1) ? s1 : s0);
+  else if constexpr (T == 1) hb = w[11];
+  else hb = mul_hi_u32(w[11], 1u << (33 - T));  // == w[11] >> (T - 1)
+  // xt already holds table base + bank offset; the three fields do not overlap
+  uint32_t addr;
+  asm("add.u32 %0, %1, %2;" : "=r"(addr) : "r"(d & 0x1FF80u), "r"(hb & 2u));
+  addr += xt;
+  // gather one fp16 entry and accumulate +-entry into fp32; the multiplier is
+  // the low (even T) or high (odd T) half of S
+  if constexpr (T & 1)
+    asm volatile(
+        "{\n\t.reg .b16 h, lo, hi;\n\t"
+        "ld.shared.u16 h, [%1];\n\t"
+        "mov.b32 {lo, hi}, %2;\n\t"
+        "fma.rn.f32.f16 %0, h, hi, %0;\n\t}"
+        : "+f"(acc) : "r"(addr), "r"(S));
+  else
+    asm volatile(
+        "{\n\t.reg .b16 h, lo, hi;\n\t"
+        "ld.shared.u16 h, [%1];\n\t"
+        "mov.b32 {lo, hi}, %2;\n\t"
+        "fma.rn.f32.f16 %0, h, lo, %0;\n\t}"
+        : "+f"(acc) : "r"(addr), "r"(S));
 }
 
 template <int T, int TPW>
 __device__ __forceinline__ void steps(const uint32_t (&w)[TPW][12], uint32_t tab,
                                       uint32_t lane4, uint32_t ones, float (&acc)[TPW]) {
   if constexpr (T < 32) {
-    const uint32_t xt = lane4 ^ (uint32_t)(T << 2);  // bank of group T ^ lane
+    const uint32_t xt = tab + (lane4 ^ (uint32_t)(T << 2));  // base + bank of group T ^ lane
 #pragma unroll
     for (int u = 0; u < TPW; ++u) {
       // +-1.0h multipliers of positions 2q, 2q+1 (sign bits at 15-q, 31-q)
       const uint32_t S = ((w[u][10] << (T >> 1)) & 0x80008000u) | ones;
-      lookup<T>(w[u], xt, S, tab, acc[u]);
+      lookup<T>(w[u], xt, S, acc[u]);
     }
     steps<T + 1, TPW>(w, tab, lane4, ones, acc);
   }

@@ -141,7 +141,7 @@ struct MmaParams {
 };
 
 template <int N, int NS>
-__global__ void __launch_bounds__(128, 1) dq_mma_kernel(MmaParams P) {
+__global__ void __launch_bounds__(128) dq_mma_kernel(MmaParams P) {
   constexpr int TB = N * 128;  // B tile bytes
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-align the carve-up (SWIZZLE_128B operands need 1024 B alignment)
@@ -274,8 +274,13 @@ __global__ void __launch_bounds__(128, 1) dq_mma_kernel(MmaParams P) {
 }
 
 template <int N, int NS>
+constexpr int dq_smem() {
+  return 1024 + 2 * 16384 + NS * (N * 128 + kMmaTileA) + (NS + 2) * 8 + 16;
+}
+
+template <int N, int NS>
 static int launch_dq(const MmaParams& P, const MmaShape& S, int splits, cudaStream_t s) {
-  const int smem = 1024 + 2 * 16384 + NS * (N * 128 + kMmaTileA) + (NS + 2) * 8 + 16;
+  const int smem = dq_smem<N, NS>();
   static int configured_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -290,8 +295,23 @@ static int launch_dq(const MmaParams& P, const MmaShape& S, int splits, cudaStre
   return MSG_OK;
 }
 
+constexpr int kDqStages = 4;
+
+static int dq_smem_for(int64_t npad) {
+  switch (npad) {
+    case 16: return dq_smem<16, kDqStages>();
+    case 32: return dq_smem<32, kDqStages>();
+    case 64: return dq_smem<64, kDqStages>();
+    case 128: return dq_smem<128, kDqStages>();
+  }
+  return dq_smem<256, kDqStages>();
+}
+
+// k-splits: enough CTAs to fill every SM with as many resident CTAs as shared
+// memory allows (up to 4), each split at least 4 k tiles long
 static int mma_splits(const MmaShape& S) {
-  int64_t sp = std::max<int64_t>(1, (int64_t)sm_count() / std::max<int64_t>(1, S.mt));
+  const int per_sm = std::max(1, std::min(4, (227 * 1024) / dq_smem_for(S.npad)));
+  int64_t sp = std::max<int64_t>(1, (int64_t)sm_count() * per_sm / std::max<int64_t>(1, S.mt));
   return (int)std::min<int64_t>(sp, std::max<int64_t>(1, S.kt / 4));
 }
 
@@ -349,11 +369,11 @@ extern "C" int msg_dequant_mma(const uint8_t* wmma, int64_t m, int64_t k, const 
   P.sub_hi = (float)(-(64.0 + off));
   int e;
   switch (S.npad) {
-    case 16: e = launch_dq<16, 8>(P, S, splits, s); break;
-    case 32: e = launch_dq<32, 8>(P, S, splits, s); break;
-    case 64: e = launch_dq<64, 6>(P, S, splits, s); break;
-    case 128: e = launch_dq<128, 5>(P, S, splits, s); break;
-    default: e = launch_dq<256, 4>(P, S, splits, s); break;
+    case 16: e = launch_dq<16, kDqStages>(P, S, splits, s); break;
+    case 32: e = launch_dq<32, kDqStages>(P, S, splits, s); break;
+    case 64: e = launch_dq<64, kDqStages>(P, S, splits, s); break;
+    case 128: e = launch_dq<128, kDqStages>(P, S, splits, s); break;
+    default: e = launch_dq<256, kDqStages>(P, S, splits, s); break;
   }
   if (e) return e;
   return launch_finish_plain(partial, splits, m, b, y, y_dtype, s);
