@@ -140,18 +140,31 @@ struct MmaParams {
   float sub_lo, sub_hi;  // dequant constants: v = h - sub (lo lanes), v = h/16 - sub (hi lanes)
 };
 
+constexpr int kNA = 3;  // dequantised A operand buffers
+
+// Warp-specialised pipeline (256 threads):
+//   warp 0 lane 0  : TMA producer -- packed W tile + swizzled X^T tile per k step
+//                    into an NS-deep ring (full/empty mbarriers);
+//   warp 1 lane 0  : MMA issuer   -- 4 x tcgen05.mma (K=16) per k step, commits
+//                    release the A operand buffer and the ring slot;
+//   warps 4..7     : dequantisers -- one row each, int4 -> fp16 (magic numbers)
+//                    into one of kNA SW128 K-major operand buffers; afterwards
+//                    the TMEM -> register -> global epilogue (warp w reads TMEM
+//                    lanes 32*(w%4)..+31).
 template <int N, int NS>
-__global__ void __launch_bounds__(128) dq_mma_kernel(MmaParams P) {
+__global__ void __launch_bounds__(256, 1) dq_mma_kernel(MmaParams P) {
   constexpr int TB = N * 128;  // B tile bytes
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-align the carve-up (SWIZZLE_128B operands need 1024 B alignment)
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* opA = smem;                              // [2][16 KiB]
-  uint8_t* stB = opA + 2 * 16384;                   // [NS][TB]
+  uint8_t* opA = smem;                              // [kNA][16 KiB]
+  uint8_t* stB = opA + kNA * 16384;                 // [NS][TB]
   uint8_t* stA = stB + NS * TB;                     // [NS][4 KiB]
-  uint64_t* full = reinterpret_cast<uint64_t*>(stA + NS * kMmaTileA);  // [NS]
-  uint64_t* done = full + NS;                                           // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 2);
+  uint64_t* full = reinterpret_cast<uint64_t*>(stA + NS * kMmaTileA);  // [NS] TMA landed
+  uint64_t* empty = full + NS;                      // [NS] slot consumed (MMA + dequant)
+  uint64_t* afull = empty + NS;                     // [kNA] operand written
+  uint64_t* aempty = afull + kNA;                   // [kNA] operand consumed by MMA
+  uint64_t* accf = aempty + kNA;                    // accumulator complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t mt = blockIdx.x, split = blockIdx.y;
@@ -160,16 +173,22 @@ __global__ void __launch_bounds__(128) dq_mma_kernel(MmaParams P) {
   const int nloc = (int)std::max<int64_t>(0, kt1 - kt0);
   constexpr uint32_t kCols = N < 32 ? 32 : N;
 
-  if (warp == 0) {
+  if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
                  "n"(kCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1);
-    mbar_init(&done[0], 1);
-    mbar_init(&done[1], 1);
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1 + 128);  // MMA commit + 128 dequant threads
+    }
+    for (int i = 0; i < kNA; ++i) {
+      mbar_init(&afull[i], 128);
+      mbar_init(&aempty[i], 1);
+    }
+    mbar_init(accf, 1);
     fence_mbar_init();
   }
   tc_fence_before();
@@ -177,38 +196,58 @@ __global__ void __launch_bounds__(128) dq_mma_kernel(MmaParams P) {
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  auto issue = [&](int i) {  // local k tile i -> ring slot i % NS (thread 0)
-    const int slot = i % NS;
-    const int64_t kt = kt0 + i;
-    mbar_expect_tx(&full[slot], kMmaTileA + TB);
-    bulk_g2s(stA + slot * kMmaTileA, P.wt + (mt * P.kt_total + kt) * kMmaTileA, kMmaTileA,
-             &full[slot]);
-    bulk_g2s(stB + slot * TB, P.xt + kt * TB, TB, &full[slot]);
-  };
-  if (tid == 0)
-    for (int i = 0; i < NS && i < nloc; ++i) issue(i);
-
-  // idesc: D f32, A/B f16, both K-major, N, M = 128
-  constexpr uint32_t idesc = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-  const __half2 sub_lo = __float2half2_rn(P.sub_lo);
-  const __half2 sub_hi = __float2half2_rn(P.sub_hi);
-  const __half2 sixteenth = __float2half2_rn(1.0f / 16.0f);
-
-  for (int i = 0; i < nloc; ++i) {
-    const int slot = i % NS, buf = i & 1;
-    mbar_wait(&full[slot], (uint32_t)((i / NS) & 1));
-    if (i >= 2) mbar_wait(&done[buf], (uint32_t)(((i - 2) >> 1) & 1));
-    // ---- dequantise row `tid` of the tile into the swizzled A operand
-    {
-      const uint4* src = reinterpret_cast<const uint4*>(stA + slot * kMmaTileA + tid * 32);
+  if (warp == 0) {
+    // ---------------- TMA producer
+    if (lane == 0) {
+      for (int i = 0; i < nloc; ++i) {
+        const int slot = i % NS;
+        if (i >= NS) mbar_wait(&empty[slot], (uint32_t)(((i / NS) - 1) & 1));
+        const int64_t kt = kt0 + i;
+        mbar_expect_tx(&full[slot], kMmaTileA + TB);
+        bulk_g2s(stA + slot * kMmaTileA, P.wt + (mt * P.kt_total + kt) * kMmaTileA, kMmaTileA,
+                 &full[slot]);
+        bulk_g2s(stB + slot * TB, P.xt + kt * TB, TB, &full[slot]);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc =
+          (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+      for (int i = 0; i < nloc; ++i) {
+        const int slot = i % NS, buf = i % kNA;
+        mbar_wait(&full[slot], (uint32_t)((i / NS) & 1));  // B tile landed (TMA)
+        mbar_wait(&afull[buf], (uint32_t)((i / kNA) & 1));
+        tc_fence_after();
+        const uint64_t ad = umma_desc_sw128(smem_u32(opA + buf * 16384));
+        const uint64_t bd = umma_desc_sw128(smem_u32(stB + slot * TB));
+#pragma unroll
+        for (int ks = 0; ks < kMmaBK / 16; ++ks)  // K = 16 per instruction = 32 bytes
+          mma_f16(tmem, ad + 2 * ks, bd + 2 * ks, idesc, (i > 0 || ks > 0) ? 1u : 0u);
+        mma_commit(&aempty[buf]);
+        mma_commit(&empty[slot]);
+      }
+      if (nloc > 0) mma_commit(accf);
+    }
+  } else if (warp >= 4) {
+    // ---------------- dequantisers, then epilogue
+    const int r = tid - 128;  // tile row
+    const __half2 sub_lo = __float2half2_rn(P.sub_lo);
+    const __half2 sub_hi = __float2half2_rn(P.sub_hi);
+    const __half2 sixteenth = __float2half2_rn(1.0f / 16.0f);
+    for (int i = 0; i < nloc; ++i) {
+      const int slot = i % NS, buf = i % kNA;
+      mbar_wait(&full[slot], (uint32_t)((i / NS) & 1));
+      const uint4* src = reinterpret_cast<const uint4*>(stA + slot * kMmaTileA + r * 32);
       const uint4 p0 = src[0], p1 = src[1];
+      mbar_arrive(&empty[slot]);  // packed A copied out
+      if (i >= kNA) mbar_wait(&aempty[buf], (uint32_t)(((i / kNA) - 1) & 1));
       const uint32_t words[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
-      uint8_t* dst_row = opA + buf * 16384 + (tid >> 3) * 1024 + (tid & 7) * 128;
+      uint8_t* dst_row = opA + buf * 16384 + (r >> 3) * 1024 + (r & 7) * 128;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {  // 16-byte chunk c = k 8c..8c+7 = word c
         uint32_t w = words[c];
         uint32_t h[4];
-        // nibbles (pos 0,4) = (k0,k1): low lanes; (1,5) = (k2,k3): x16 lanes; then >> 8
         h[0] = (w & 0x000F000Fu) | 0x64006400u;
         h[1] = (w & 0x00F000F0u) | 0x64006400u;
         w >>= 8;
@@ -220,62 +259,49 @@ __global__ void __launch_bounds__(128) dq_mma_kernel(MmaParams P) {
         __half2 v3 = __hfma2(*reinterpret_cast<__half2*>(&h[3]), sixteenth, sub_hi);
         uint4 o = make_uint4(*reinterpret_cast<uint32_t*>(&v0), *reinterpret_cast<uint32_t*>(&v1),
                              *reinterpret_cast<uint32_t*>(&v2), *reinterpret_cast<uint32_t*>(&v3));
-        *reinterpret_cast<uint4*>(dst_row + ((c ^ (tid & 7)) * 16)) = o;
+        *reinterpret_cast<uint4*>(dst_row + ((c ^ (r & 7)) * 16)) = o;
       }
+      fence_proxy_async();  // generic smem writes -> visible to the tensor core
+      mbar_arrive(&afull[buf]);
     }
-    fence_proxy_async();  // generic smem writes -> visible to the tensor core (async proxy)
-    __syncthreads();
-    if (tid == 0) {
+    // ---------------- epilogue: TMEM -> registers -> fp32 partials
+    const int quarter = warp & 3;
+    const int64_t row = mt * kMmaBM + quarter * 32 + lane;
+    float* dst = P.partial + (split * P.m + row) * P.b;
+    if (nloc > 0) {
+      mbar_wait(accf, 0);
       tc_fence_after();
-      const uint64_t ad = umma_desc_sw128(smem_u32(opA + buf * 16384));
-      const uint64_t bd = umma_desc_sw128(smem_u32(stB + slot * TB));
 #pragma unroll
-      for (int ks = 0; ks < kMmaBK / 16; ++ks)  // K = 16 per instruction = 32 bytes
-        mma_f16(tmem, ad + 2 * ks, bd + 2 * ks, idesc, (i > 0 || ks > 0) ? 1u : 0u);
-      mma_commit(&done[buf]);
-      // slot of tile i-1 is free once its MMAs are done: refill with tile i-1+NS
-      if (i >= 1 && i - 1 + NS < nloc) {
-        mbar_wait(&done[(i - 1) & 1], (uint32_t)(((i - 1) >> 1) & 1));
-        issue(i - 1 + NS);
+      for (int c0 = 0; c0 < N; c0 += 16) {
+        uint32_t v[16];
+        const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+            "%13,%14,%15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+              "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+              "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (row < P.m) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            if (c0 + e < P.b) dst[c0 + e] = __uint_as_float(v[e]);
+        }
       }
+    } else if (row < P.m) {
+      for (int64_t e = 0; e < P.b; ++e) dst[e] = 0.f;
     }
-  }
-  // ---- epilogue: TMEM -> registers -> fp32 partials
-  const int64_t row = mt * kMmaBM + warp * 32 + lane;
-  float* dst = P.partial + (split * P.m + row) * P.b;
-  if (nloc > 0) {
-    mbar_wait(&done[(nloc - 1) & 1], (uint32_t)(((nloc - 1) >> 1) & 1));
-    tc_fence_after();
-#pragma unroll
-    for (int c0 = 0; c0 < N; c0 += 16) {
-      uint32_t r[16];
-      const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-          "%14,%15}, [%16];"
-          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-            "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-            "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (row < P.m) {
-#pragma unroll
-        for (int e = 0; e < 16; ++e)
-          if (c0 + e < P.b) dst[c0 + e] = __uint_as_float(r[e]);
-      }
-    }
-  } else if (row < P.m) {
-    for (int64_t e = 0; e < P.b; ++e) dst[e] = 0.f;
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0)
+  if (warp == 2)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols));
 }
 
 template <int N, int NS>
 constexpr int dq_smem() {
-  return 1024 + 2 * 16384 + NS * (N * 128 + kMmaTileA) + (NS + 2) * 8 + 16;
+  return 1024 + kNA * 16384 + NS * (N * 128 + kMmaTileA) + (2 * NS + 2 * kNA + 1) * 8 + 16;
 }
 
 template <int N, int NS>
@@ -290,7 +316,7 @@ static int launch_dq(const MmaParams& P, const MmaShape& S, int splits, cudaStre
     configured_dev = dev;
   }
   dim3 grid((unsigned)S.mt, (unsigned)splits);
-  dq_mma_kernel<N, NS><<<grid, 128, smem, s>>>(P);
+  dq_mma_kernel<N, NS><<<grid, 256, smem, s>>>(P);
   MSG_LAUNCH_CHECK();
   return MSG_OK;
 }
