@@ -529,6 +529,7 @@ __global__ void __launch_bounds__(256) fused_finish_kernel(
     const void* q, int q_dtype, void* y, int y_dtype) {
   constexpr int OPB = 256 / SG;  // outputs per block
   __shared__ float red[SG][OPB];
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the LUT kernel's partials are complete
   const int64_t nb = k / d;
   const int tail = (int)(k - nb * d);
   const int64_t total = m * b;
@@ -829,9 +830,21 @@ int launch_finish(const float* partial, int S, int64_t m, int64_t b, int64_t k, 
   const int opb = 256 / sg;
   const int grid =
       (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, opb), (int64_t)sm_count() * 16));
+  // Programmatic dependent launch: the finish grid is set up while the LUT
+  // kernel drains and waits (griddepcontrol.wait) for its results.
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
 #define MSG_FIN(G)                                                                            \
-  fused_finish_kernel<G><<<grid, 256, 0, s>>>(partial, S, m, b, k, d, tailp, tv, x, x_dtype,  \
-                                              scale_mode, q, q_dtype, y, y_dtype)
+  MSG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fused_finish_kernel<G>, partial, S, m, b, k, d,    \
+                                    tailp, tv, x, x_dtype, scale_mode, q, q_dtype, y, y_dtype))
   switch (sg) {
     case 1: MSG_FIN(1); break;
     case 2: MSG_FIN(2); break;
