@@ -70,11 +70,13 @@ extern "C" {
 #define MSG_FLAG_FORCE_GENERIC 4  /* global-memory table path (any d, width, dtype)        */
 #define MSG_FLAG_LUT_PHASE_ONLY 8 /* measurement: launch only the fused LUT kernel (Y untouched) */
 #define MSG_FLAG_NO_LANE      16  /* do not use the b=1 lane kernel (use the row-block kernel) */
+#define MSG_FLAG_PAIR         32  /* opt-in: double-buffered 2-group row-block kernel (slower on B200, kept for study) */
 
 /* weight layouts produced by msg_repack */
 #define MSG_LAYOUT_NONE 0  /* reference row-major nibbles only      */
 #define MSG_LAYOUT_QUAD 1  /* quad planes for the fused LUT kernel  */
 #define MSG_LAYOUT_LANE 2  /* lane-rotated 32-group chunks for the b=1, d=3 GEMV kernel */
+#define MSG_LAYOUT_PAIR 3  /* quad planes, half-quad pair rotation (double-buffered kernel) */
 
 MSG_API const char* msg_last_error(void);
 /* diagnostics: per-CTA trace records {smid, t_start_ns, t_end_ns, units} of

@@ -24,7 +24,8 @@ F32, F16, F64, I32, I64, U8, I8, I16, BF16 = range(9)
 SCALE_NONE, SCALE_PER_ROW, SCALE_PER_GROUP = 0, 1, 2
 FLAG_F32_ENTRIES, FLAG_NO_SYMMETRY, FLAG_FORCE_GENERIC, FLAG_LUT_PHASE_ONLY = 1, 2, 4, 8
 FLAG_NO_LANE = 16
-LAYOUT_NONE, LAYOUT_QUAD, LAYOUT_LANE = 0, 1, 2
+FLAG_PAIR = 32
+LAYOUT_NONE, LAYOUT_QUAD, LAYOUT_LANE, LAYOUT_PAIR = 0, 1, 2, 3
 
 EXPORTS = (
     "msg_last_error", "msg_version", "msg_device_sm_count", "msg_pack_codes",

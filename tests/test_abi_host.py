@@ -55,9 +55,12 @@ def test_plan_configs_take_fused_symmetric_path(m, k, b, d):
     st, lay, sym, ws = _plan(m, k, b, d)
     want = _lib.LAYOUT_LANE if (b == 1 and d == 3) else _lib.LAYOUT_QUAD
     assert st == 0 and lay == want and sym == 1 and ws > 0
-    # the row-block kernel remains selectable for the GEMV shapes
+    # the row-block kernels remain selectable for the GEMV shapes
     st, lay, sym, ws = _plan(m, k, b, d, flags=_lib.FLAG_NO_LANE)
     assert st == 0 and lay == _lib.LAYOUT_QUAD
+    # the double-buffered pair kernel is opt-in
+    st, lay, sym, ws = _plan(m, k, b, d, flags=_lib.FLAG_NO_LANE | _lib.FLAG_PAIR)
+    assert st == 0 and lay == _lib.LAYOUT_PAIR
 
 
 def test_plan_routes_to_generic():
