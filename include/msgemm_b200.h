@@ -71,6 +71,9 @@ extern "C" {
 #define MSG_FLAG_LUT_PHASE_ONLY 8 /* measurement: launch only the fused LUT kernel (Y untouched) */
 #define MSG_FLAG_NO_LANE      16  /* do not use the b=1 lane kernel (use the row-block kernel) */
 #define MSG_FLAG_PAIR         32  /* opt-in: double-buffered 2-group row-block kernel (slower on B200, kept for study) */
+#define MSG_FLAG_STATIC_WEIGHTS 64 /* the repacked weights were not written by the kernel launched just
+                                      before on this stream: the LUT kernel may start streaming them
+                                      before that kernel completes (programmatic dependent launch) */
 
 /* weight layouts produced by msg_repack */
 #define MSG_LAYOUT_NONE 0  /* reference row-major nibbles only      */

@@ -25,6 +25,7 @@ SCALE_NONE, SCALE_PER_ROW, SCALE_PER_GROUP = 0, 1, 2
 FLAG_F32_ENTRIES, FLAG_NO_SYMMETRY, FLAG_FORCE_GENERIC, FLAG_LUT_PHASE_ONLY = 1, 2, 4, 8
 FLAG_NO_LANE = 16
 FLAG_PAIR = 32
+FLAG_STATIC_WEIGHTS = 64
 LAYOUT_NONE, LAYOUT_QUAD, LAYOUT_LANE, LAYOUT_PAIR = 0, 1, 2, 3
 
 EXPORTS = (

@@ -161,6 +161,13 @@ __device__ __forceinline__ unsigned int sm_id() {
 // ----------------------------------------------------------------------------
 // mbarrier + cp.async.bulk (TMA bulk copy) helpers
 // ----------------------------------------------------------------------------
+// Programmatic dependent launch (PDL): wait for the preceding grid's results
+// / let the next grid start its prologue.  No-ops without the launch attribute.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

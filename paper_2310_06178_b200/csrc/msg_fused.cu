@@ -49,7 +49,7 @@ int64_t lane_tail_offset(int64_t m, int64_t k);
 int64_t lane_partial_slices(int64_t m, int64_t k);
 int lane_repack(const uint8_t* packed, int64_t m, int64_t k, uint8_t* out, cudaStream_t s);
 int launch_lane(const uint8_t* wrep, int64_t m, int64_t k, const double* values, double beta,
-                const void* x, int x_dtype, float* partial, cudaStream_t s);
+                const void* x, int x_dtype, float* partial, bool early, cudaStream_t s);
 
 static inline int64_t align256(int64_t v) { return (v + 255) / 256 * 256; }
 
@@ -1004,7 +1004,8 @@ int msg_gemm(const uint8_t* packed, const uint8_t* wrep, int64_t m, int64_t k, i
   for (int c = 0; c < 16; ++c) tv.v[c] = (float)values[c];
   float* partial = reinterpret_cast<float*>(workspace);
   if (p.lane) {
-    if (int e = launch_lane(wrep, m, k, values, beta, x, x_dtype, partial, s)) return e;
+    if (int e = launch_lane(wrep, m, k, values, beta, x, x_dtype, partial,
+                                (flags & MSG_FLAG_STATIC_WEIGHTS) != 0, s)) return e;
     if (flags & MSG_FLAG_LUT_PHASE_ONLY) return MSG_OK;
     const uint16_t* tailp =
         (k % 3) ? reinterpret_cast<const uint16_t*>(wrep + lane_tail_offset(m, k)) : nullptr;

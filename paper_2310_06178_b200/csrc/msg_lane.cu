@@ -129,17 +129,13 @@ struct LaneParams {
   float* partial;  // [nchunk][m]
   TraceRec* trace;  // per-CTA trace records or nullptr
   uint32_t ones;    // 0x3C003C00: two fp16 +1.0
+  int early;        // MSG_FLAG_STATIC_WEIGHTS: stream weights before griddepcontrol.wait
 };
 
 constexpr int kLaneThreads = 512;
 
-template <typename XT> __device__ __forceinline__ float ldx_l(const void* p, int64_t i);
-template <> __device__ __forceinline__ float ldx_l<float>(const void* p, int64_t i) {
-  return __ldg(reinterpret_cast<const float*>(p) + i);
-}
-template <> __device__ __forceinline__ float ldx_l<__half>(const void* p, int64_t i) {
-  return __half2float(reinterpret_cast<const __half*>(p)[i]);
-}
+__device__ __forceinline__ float to_f(float v) { return v; }
+__device__ __forceinline__ float to_f(__half v) { return __half2float(v); }
 
 // One lookup at position T: the 10-bit row field lands at byte-offset bits
 // 7..16 via one funnel shift, the half select at bit 1, the bank offset
@@ -234,56 +230,60 @@ __global__ void __launch_bounds__(kLaneThreads, 1) lane_lut_kernel(LaneParams P)
   fence_mbar_init();
   __syncwarp();
 
-  // tile of this warp for (superbatch sb, q): sb*SB + warp*TPW + q
+  // Issue cursor (lane-uniform, no division on the hot path): chunk nc,
+  // superbatch ns within it, tile nq of this warp's batch; nu = linear unit.
+  // Tile of this warp for (ns, nq) is ns*SB + warp*TPW + nq.
   uint32_t issued = 0, consumed = 0;  // per-warp ring counters (lane-uniform)
-  int64_t next_u = u_begin;           // issue cursor: superbatch
-  int next_q = 0;                     //               and tile within the warp's batch
-  auto tile_of = [&](int64_t uu, int q, const uint8_t*& src) -> bool {
-    const int64_t c = uu / nsb, sb = uu - c * nsb;
-    const int64_t t = sb * SB + warp * TPW + q;
-    if (t >= P.ntiles) return false;
-    src = P.body + (c * P.ntiles + t) * kTileBytes;
-    return true;
-  };
-  // keep kRing tiles of this warp in flight, in consumption order (lane 0)
+  int64_t nu = u_begin, nc = u_begin / nsb, ns = u_begin - (u_begin / nsb) * nsb;
+  int nq = 0;
+  // keep kRing tiles of this warp in flight, in consumption order (lane 0 issues)
   auto refill = [&]() {
-    if (lane == 0) {
-      while (issued - consumed < (uint32_t)kRing && next_u < u_end) {
-        const uint8_t* src;
-        const bool ok = tile_of(next_u, next_q, src);
-        if (ok) {
+    while (issued - consumed < (uint32_t)kRing && nu < u_end) {
+      const int64_t t = ns * SB + warp * TPW + nq;
+      if (t < P.ntiles) {
+        if (lane == 0) {
           const int slot = issued % kRing;
           fence_proxy_async();
           mbar_expect_tx(&bars[slot], kTileBytes);
-          bulk_g2s(ring + slot * kTileBytes, src, kTileBytes, &bars[slot]);
-          ++issued;
+          bulk_g2s(ring + slot * kTileBytes, P.body + (nc * P.ntiles + t) * kTileBytes,
+                   kTileBytes, &bars[slot]);
         }
-        if (++next_q == TPW) { next_q = 0; ++next_u; }
+        ++issued;
+      }
+      if (++nq == TPW) {
+        nq = 0;
+        ++nu;
+        if (++ns == nsb) { ns = 0; ++nc; }
       }
     }
-    issued = __shfl_sync(0xffffffffu, issued, 0);
-    next_u = __shfl_sync(0xffffffffu, next_u, 0);
-    next_q = __shfl_sync(0xffffffffu, next_q, 0);
   };
 
-  auto load_x = [&](int64_t c, float& x0, float& x1, float& x2) {
-    x0 = x1 = x2 = 0.f;
+  // activations are prefetched as raw XT values and converted at the build,
+  // so the load latency is not exposed where the prefetch is issued
+  auto load_x = [&](int64_t c, XT& x0, XT& x1, XT& x2) {
+    x0 = x1 = x2 = XT(0.f);
     const int64_t g = c * 32 + lane;
     if (c < P.nchunk && g < P.nb) {
-      x0 = ldx_l<XT>(P.x, 3 * g);
-      x1 = ldx_l<XT>(P.x, 3 * g + 1);
-      x2 = ldx_l<XT>(P.x, 3 * g + 2);
+      const XT* xp = reinterpret_cast<const XT*>(P.x) + 3 * g;
+      x0 = xp[0];
+      x1 = xp[1];
+      x2 = xp[2];
     }
   };
-  float xn0, xn1, xn2;
+  XT xn0, xn1, xn2;
+  // Launched with PDL: the prologue overlaps the previous kernel's tail.  The
+  // weight stream may start before the wait only if the previous kernel did
+  // not write it; x and the partials are touched only after the wait.
+  if (P.early) refill();
+  griddep_wait();
+  if (!P.early) refill();
   load_x(u_begin / nsb, xn0, xn1, xn2);
-  refill();  // start streaming before the first table build
 
   int64_t u = u_begin;
   while (u < u_end) {
     const int64_t c = u / nsb;
     const int64_t sb_end = std::min<int64_t>(u_end, (c + 1) * nsb);  // this chunk's share
-    const float x0 = xn0, x1 = xn1, x2 = xn2;
+    const float x0 = to_f(xn0), x1 = to_f(xn1), x2 = to_f(xn2);
     load_x(c + 1, xn0, xn1, xn2);  // prefetch the next chunk's activations
     // ---- build chunk c's 32 bank-private half tables (groups beyond nb get
     // x = 0, i.e. all-zero tables, so padded positions contribute nothing)
@@ -396,8 +396,17 @@ static int launch_lane_t(const LaneParams& P, cudaStream_t s) {
   const int64_t nsb = (P.ntiles + TPW * kNW - 1) / (TPW * kNW);
   const int64_t U = P.nchunk * nsb;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(U, sm_count()));
-  lane_lut_kernel<XT, TPW><<<grid, kLaneThreads, kLaneSmem, s>>>(P);
-  MSG_LAUNCH_CHECK();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kLaneThreads);
+  cfg.dynamicSmemBytes = kLaneSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  MSG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, lane_lut_kernel<XT, TPW>, P));
   return MSG_OK;
 }
 
@@ -411,7 +420,7 @@ static int launch_lane_x(const LaneParams& P, cudaStream_t s) {
 }
 
 int launch_lane(const uint8_t* wrep, int64_t m, int64_t k, const double* values, double beta,
-                const void* x, int x_dtype, float* partial, cudaStream_t s) {
+                const void* x, int x_dtype, float* partial, bool early, cudaStream_t s) {
   LaneLayout L = lane_layout(m, k);
   LaneParams P{};
   P.body = wrep + L.body_off;
@@ -425,6 +434,7 @@ int launch_lane(const uint8_t* wrep, int64_t m, int64_t k, const double* values,
   P.partial = partial;
   P.trace = trace_buffer();
   P.ones = 0x3C003C00u;
+  P.early = early ? 1 : 0;
   if (x_dtype == MSG_F16) return launch_lane_x<__half>(P, s);
   return launch_lane_x<float>(P, s);
 }

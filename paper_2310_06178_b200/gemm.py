@@ -163,8 +163,13 @@ def msgemm(pwm: PackedWeightMatrix, X, d: int, budget: int = DEFAULT_BUDGET,
         Y = t.empty((m, b), dtype=y_dt, device=dev)
     y_code = _lib.dtype_code(y_dt)
     if m and b:
-        wrep = (pwm.device_layout(dev, d, layout.value, sym.value)
-                if layout.value != _lib.LAYOUT_NONE else None)
+        wrep = None
+        if layout.value != _lib.LAYOUT_NONE:
+            # a layout built by an earlier call is not written by the kernel that
+            # precedes this one: the LUT kernel may prefetch it under PDL
+            if pwm.has_device_layout(dev, d, layout.value, sym.value):
+                flags |= _lib.FLAG_STATIC_WEIGHTS
+            wrep = pwm.device_layout(dev, d, layout.value, sym.value)
         ws = _lib.workspace(ws_bytes.value, dev)
         _lib.check(lib.msg_gemm(
             _lib.ptr(pwm.device_data(dev)), _lib.ptr(wrep), m, k, pwm.width, vals,

@@ -83,6 +83,10 @@ class PackedWeightMatrix:
             cache[key] = _lib.to_device(self.data, dev)
         return cache[key]
 
+    def has_device_layout(self, dev, d: int, layout: int, symmetric: int) -> bool:
+        """True once device_layout(...) has been built (by an earlier call)."""
+        return ("layout", dev.index, d, layout, symmetric) in self._device_cache
+
     def device_layout(self, dev, d: int, layout: int, symmetric: int):
         """The K3-repacked layout for depth d on `dev` (built once)."""
         cache = self._device_cache
