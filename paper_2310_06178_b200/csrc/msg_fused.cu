@@ -751,8 +751,16 @@ __global__ void __launch_bounds__(256) fused_finish_kernel(
     const int64_t t = t0 + og;
     float s = 0.f;
     if (t < total) {
+      if (scale_mode == MSG_SCALE_PER_GROUP) {
+        // slice sl is scale group sl: q is (m, S) row-major (packing.py:29-36)
+        const int64_t qi = (t / b) * S;
+#pragma unroll 4
+        for (int sl = sg; sl < S; sl += SG)
+          s = fmaf(load_as<float>(q, q_dtype, qi + sl), __ldcg(partial + (int64_t)sl * total + t), s);
+      } else {
 #pragma unroll 8
-      for (int sl = sg; sl < S; sl += SG) s += __ldcg(partial + (int64_t)sl * total + t);
+        for (int sl = sg; sl < S; sl += SG) s += __ldcg(partial + (int64_t)sl * total + t);
+      }
     }
     if constexpr (SG > 1) {
       red[sg][og] = s;
@@ -795,19 +803,28 @@ static bool codebook_antisymmetric(const double* v, int n, double* beta) {
   return true;
 }
 
-static bool fused_eligible(int width, int x_dtype, int d, int scale_mode) {
+// Per-group scales (gemm.py:75-79) run on the row-block kernels when every
+// scale group is a whole number of quads: each k-slice is then exactly one
+// scale group and the finish kernel weights slice s of row i by q[i, s].
+static bool per_group_quads(int64_t k, int d, int64_t group_size) {
+  return group_size > 0 && k % group_size == 0 && group_size % d == 0 &&
+         (group_size / d) % 4 == 0;
+}
+
+static bool fused_eligible(int width, int x_dtype, int64_t k, int d, int scale_mode,
+                           int64_t group_size) {
   return width == 4 && (x_dtype == MSG_F16 || x_dtype == MSG_F32) && d >= 1 && d <= 3 &&
-         scale_mode != MSG_SCALE_PER_GROUP;
+         (scale_mode != MSG_SCALE_PER_GROUP || per_group_quads(k, d, group_size));
 }
 
 static int rpt_for(int bc) { return bc == 8 ? 16 : 32; }
 
 static FusedPlan fused_plan(int64_t m, int64_t k, int width, const double* values, int x_dtype,
-                            int64_t b, int d, int scale_mode, int flags) {
+                            int64_t b, int d, int scale_mode, int64_t group_size, int flags) {
   FusedPlan p{};
   p.ok = false;
   if (flags & MSG_FLAG_FORCE_GENERIC) return p;
-  if (!fused_eligible(width, x_dtype, d, scale_mode)) return p;
+  if (!fused_eligible(width, x_dtype, k, d, scale_mode, group_size)) return p;
   if (m <= 0 || b <= 0 || k / d == 0) return p;
   double beta = 0;
   p.sym = !(flags & MSG_FLAG_NO_SYMMETRY) && codebook_antisymmetric(values, 16, &beta);
@@ -842,6 +859,7 @@ static FusedPlan fused_plan(int64_t m, int64_t k, int width, const double* value
   int64_t S = std::max<int64_t>(1, sm_count() / std::max<int64_t>(1, base));
   S = std::min<int64_t>(S, p.L.nq);
   p.quads_per_slice = (int)ceil_div(p.L.nq, S);
+  if (scale_mode == MSG_SCALE_PER_GROUP) p.quads_per_slice = (int)(group_size / d / 4);
   p.S = (int)ceil_div(p.L.nq, p.quads_per_slice);
   int64_t ql = std::max<int64_t>(1, std::min<int64_t>(budget / quad_bytes(bc), p.quads_per_slice));
   // staged activations: at most 2 per thread per round
@@ -969,7 +987,7 @@ int msg_gemm_plan(int64_t m, int64_t k, int width, const double* values, int x_d
                   int d, int scale_mode, int64_t group_size, int flags, int* layout_out,
                   int* symmetric_out, int64_t* ws_out) {
   if (int e = validate_gemm(m, k, width, x_dtype, b, d, scale_mode, group_size)) return e;
-  FusedPlan p = fused_plan(m, k, width, values, x_dtype, b, d, scale_mode, flags);
+  FusedPlan p = fused_plan(m, k, width, values, x_dtype, b, d, scale_mode, group_size, flags);
   if (p.ok) {
     *layout_out = p.lane ? MSG_LAYOUT_LANE : (p.pair ? MSG_LAYOUT_PAIR : MSG_LAYOUT_QUAD);
     *symmetric_out = p.sym ? 1 : 0;
@@ -990,7 +1008,7 @@ int msg_gemm(const uint8_t* packed, const uint8_t* wrep, int64_t m, int64_t k, i
   if (dtype_size(y_dtype) == 0) return fail(MSG_ERR_UNSUPPORTED, "bad output dtype %d", y_dtype);
   cudaStream_t s = as_stream(stream);
   CodebookParam cb = make_codebook(values, width);
-  FusedPlan p = fused_plan(m, k, width, values, x_dtype, b, d, scale_mode, flags);
+  FusedPlan p = fused_plan(m, k, width, values, x_dtype, b, d, scale_mode, group_size, flags);
   if (!p.ok)
     return run_generic(packed, m, k, width, cb, x, x_dtype, b, d, scale_mode, group_size, q,
                        q_dtype, y, y_dtype, workspace, ws_bytes, s);

@@ -66,7 +66,10 @@ def test_plan_configs_take_fused_symmetric_path(m, k, b, d):
 def test_plan_routes_to_generic():
     assert _plan(64, 48, 3, 4)[1] == _lib.LAYOUT_NONE                    # d=4
     assert _plan(64, 48, 3, 2, dt=_lib.I64)[1] == _lib.LAYOUT_NONE       # integer X
-    assert _plan(64, 48, 3, 2, scale=2, gs=4)[1] == _lib.LAYOUT_NONE     # per-group
+    assert _plan(64, 48, 3, 2, scale=2, gs=4)[1] == _lib.LAYOUT_NONE     # per-group, 2 groups
+    assert _plan(64, 48, 3, 2, scale=2, gs=8)[1] == _lib.LAYOUT_QUAD     # per-group, 1 quad
+    assert _plan(64, 96, 1, 3, scale=2, gs=12)[1] == _lib.LAYOUT_QUAD    # b=1: not the lane kernel
+    assert _plan(64, 40, 3, 2, scale=2, gs=16)[1] == _lib.LAYOUT_NONE    # k % group_size != 0
     assert _plan(64, 48, 3, 2, flags=_lib.FLAG_FORCE_GENERIC)[1] == _lib.LAYOUT_NONE
     assert _plan(64, 48, 3, 3, flags=_lib.FLAG_NO_SYMMETRY)[2] == 0
     custom = mg.custom_codebook([0, 1, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 17])
