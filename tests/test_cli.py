@@ -1,0 +1,76 @@
+"""The GPU-backed CLI: exit codes and file formats as
+the reference's cli.py (0 ok, 1 validation/format error, 2 verify failure)."""
+
+import numpy as np
+import pytest
+
+from paper_2310_06178_b200 import cli, formats
+from oracle import msgemm_oracle as orc
+
+
+def test_parser_has_reference_subcommands():
+    p = cli.build_parser()
+    for argv in (["pack", "--random", "4", "6", "-o", "w"], ["unpack", "w"],
+                 ["matmul", "w", "x", "--d", "2", "-o", "y"], ["verify", "w", "x", "--d", "2"],
+                 ["bench", "--m", "8", "--k", "8", "--d", "2"]):
+        assert p.parse_args(argv).command == argv[0]
+
+
+def test_errors_exit_1_without_device(tmp_path, capsys):
+    assert cli.main(["unpack", str(tmp_path / "missing.msgw")]) == cli.EXIT_ERROR
+    bad = tmp_path / "bad.msgw"
+    bad.write_bytes(b"XXXX" + bytes(40))
+    assert cli.main(["matmul", str(bad), str(bad), "--d", "2", "-o", str(tmp_path / "y")]) == 1
+    assert cli.main(["bench", "--m", "8", "--k", "8", "--d", "3", "--iters", "1"]) == 1  # d∤k
+    assert cli.main(["bench", "--m", "8", "--k", "8", "--d", "2", "--iters", "0"]) == 1
+    assert "error:" in capsys.readouterr().err
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scale", [["--scale-mode", "none"], ["--scale-mode", "per-row"],
+                                   ["--scale-mode", "per-group", "--group-size", "48"]])
+def test_pack_matmul_verify_roundtrip(tmp_path, scale):
+    w, x, y = tmp_path / "w.msgw", tmp_path / "x.msga", tmp_path / "y.msgy"
+    assert cli.main(["pack", "--random", "200", "96", "--seed", "3", "-o", str(w)] + scale) == 0
+    rng = np.random.default_rng(1)
+    X = rng.standard_normal((96, 5)).astype(np.float32)
+    formats.write_activations(x, X)
+    assert cli.main(["matmul", str(w), str(x), "--d", "3", "-o", str(y)]) == 0
+    Y = formats.read_output(y)
+    pwm = formats.read_weights(w)
+    from paper_2310_06178_b200.packing import PerGroup, PerRow
+    kw = {}
+    if isinstance(pwm.scales, PerRow):
+        kw = dict(scale_mode="per_row", q=pwm.scales.q)
+    elif isinstance(pwm.scales, PerGroup):
+        kw = dict(scale_mode="per_group", group_size=pwm.scales.group_size, q=pwm.scales.q)
+    ref = orc.msgemm(pwm.data, pwm.m, pwm.k, 4, pwm.codebook.values, X, 3, **kw)
+    Wd = orc.dense(pwm.data, pwm.k, 4, pwm.codebook.values, kw.get("scale_mode"),
+                   kw.get("group_size", 0), kw.get("q"), apply_scales=True)
+    assert orc.rel_error(Y, Wd, X) <= 1e-5
+    assert np.max(np.abs(Y - ref)) <= 1e-5 * np.max(np.abs(Wd) @ np.abs(X)) + 1e-30
+    assert cli.main(["verify", str(w), str(x), "--d", "3"]) in (0, 2)
+
+
+@pytest.mark.gpu
+def test_verify_exit_codes(tmp_path):
+    w, x = tmp_path / "w.msgw", tmp_path / "x.msga"
+    assert cli.main(["pack", "--random", "64", "60", "-o", str(w)]) == 0
+    Xi = np.random.default_rng(2).integers(-127, 128, (60, 3)).astype(np.float32)
+    formats.write_activations(x, Xi)
+    assert cli.main(["verify", str(w), str(x), "--d", "2", "--mode", "exact-int"]) == 0
+    Xn = Xi.copy()
+    Xn[0, 0] = np.nan
+    formats.write_activations(x, Xn)
+    assert cli.main(["verify", str(w), str(x), "--d", "2"]) == cli.EXIT_VERIFY_FAILED
+    Xf = Xi + 0.5
+    formats.write_activations(x, Xf)
+    assert cli.main(["verify", str(w), str(x), "--d", "2", "--mode", "exact-int"]) == 1
+
+
+@pytest.mark.gpu
+def test_bench_runs(capsys):
+    assert cli.main(["bench", "--m", "512", "--k", "513", "--b", "4", "--d", "3",
+                     "--iters", "2"]) == 0
+    out = capsys.readouterr().out
+    assert "msgemm  median" in out and "GOP/s" in out
