@@ -742,11 +742,35 @@ __global__ void __launch_bounds__(256) fused_finish_kernel(
     const void* q, int q_dtype, void* y, int y_dtype) {
   constexpr int OPB = 256 / SG;  // outputs per block
   __shared__ float red[SG][OPB];
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the LUT kernel's partials are complete
   const int64_t nb = k / d;
-  const int tail = (int)(k - nb * d);
+  const int tail = (int)(k - nb * d);  // < d <= 3 on the fused paths
   const int64_t total = m * b;
   const int og = threadIdx.x % OPB, sg = threadIdx.x / OPB;
+  // Operands that do not depend on the partials (tail weights and activations,
+  // per-row scale) are loaded before griddepcontrol.wait: the LUT kernel only
+  // writes the partials, and x / wrep / q were final before it started.
+  float tw[2] = {0.f, 0.f}, tx[2] = {0.f, 0.f}, qs = 1.f;
+  auto extras = [&](int64_t t) {
+    const int64_t i = t / b, c = t - i * b;
+    if (tail) {
+      const uint32_t tc = tailp[i];
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        if (u < tail) {
+          tw[u] = vals.v[(tc >> (4 * u)) & 0xF];
+          tx[u] = load_as<float>(x, x_dtype, (nb * d + u) * b + c);
+        }
+    }
+    if (scale_mode == MSG_SCALE_PER_ROW) qs = load_as<float>(q, q_dtype, i);
+  };
+  {
+    const int64_t t = (int64_t)blockIdx.x * OPB + og;
+    if (t < total && sg == 0) extras(t);
+  }
+  // PDL: let the next kernel on the stream (e.g. the next layer's LUT kernel)
+  // start its prologue now; then wait until the LUT kernel's partials are complete
+  griddep_launch_dependents();
+  griddep_wait();
   for (int64_t t0 = (int64_t)blockIdx.x * OPB; t0 < total; t0 += (int64_t)gridDim.x * OPB) {
     const int64_t t = t0 + og;
     float s = 0.f;
@@ -772,13 +796,11 @@ __global__ void __launch_bounds__(256) fused_finish_kernel(
       __syncthreads();
     }
     if (t < total && sg == 0) {
-      const int64_t i = t / b, c = t - i * b;
-      if (tail) {
-        uint32_t tc = tailp[i];
-        for (int u = 0; u < tail; ++u)
-          s = fmaf(vals.v[(tc >> (4 * u)) & 0xF], load_as<float>(x, x_dtype, (nb * d + u) * b + c), s);
-      }
-      if (scale_mode == MSG_SCALE_PER_ROW) s *= load_as<float>(q, q_dtype, i);
+      if (t0 != (int64_t)blockIdx.x * OPB) extras(t);
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        if (u < tail) s = fmaf(tw[u], tx[u], s);
+      if (scale_mode == MSG_SCALE_PER_ROW) s *= qs;
       store_as<float>(y, y_dtype, t, s);
     }
   }
@@ -1069,7 +1091,7 @@ int launch_finish(const float* partial, int S, int64_t m, int64_t b, int64_t k, 
   const int64_t total = m * b;
   // slice groups per output: enough loads in flight to cover the SMs
   int sg = 1;
-  while (sg < 8 && 2 * sg <= S && total * sg < (int64_t)sm_count() * 2048) sg *= 2;
+  while (sg < 32 && 2 * sg <= S && total * sg < (int64_t)sm_count() * 2048) sg *= 2;
   const int opb = 256 / sg;
   const int grid =
       (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, opb), (int64_t)sm_count() * 16));
@@ -1092,7 +1114,9 @@ int launch_finish(const float* partial, int S, int64_t m, int64_t b, int64_t k, 
     case 1: MSG_FIN(1); break;
     case 2: MSG_FIN(2); break;
     case 4: MSG_FIN(4); break;
-    default: MSG_FIN(8); break;
+    case 8: MSG_FIN(8); break;
+    case 16: MSG_FIN(16); break;
+    default: MSG_FIN(32); break;
   }
 #undef MSG_FIN
   MSG_LAUNCH_CHECK();

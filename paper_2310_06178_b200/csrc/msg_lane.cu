@@ -276,6 +276,7 @@ __global__ void __launch_bounds__(kLaneThreads, 1) lane_lut_kernel(LaneParams P)
   // not write it; x and the partials are touched only after the wait.
   if (P.early) refill();
   griddep_wait();
+  griddep_launch_dependents();  // the finish kernel may queue behind this grid
   if (!P.early) refill();
   load_x(u_begin / nsb, xn0, xn1, xn2);
 
