@@ -197,6 +197,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--split", default="rows", choices=["rows", "k"],
+                    help="N>1: shard rows (+ all-gather of Y, default) or the inner dimension "
+                         "(+ fp32 all-reduce of partial Y; splits the table build too)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -219,18 +222,29 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     cfg = CONFIGS[args.config]
-    if cfg.m % world:
-        raise SystemExit(f"m={cfg.m} not divisible by {world} ranks")
-    mr = cfg.m // world
-    r0 = rank * mr
-
-    data = weights(cfg)[r0:r0 + mr]
+    ksplit = world > 1 and args.split == "k"
     X = activations(cfg)
     exact = cfg.x_dtype == "int"
     Xh = X.astype(np.float16) if exact else X
-    xd = torch.from_numpy(Xh).to(dev)
     kw = dict(table_dtype=np.float32, out_dtype=np.float32) if exact else {}
-    y_dt = torch.float32 if exact else xd.dtype
+    if ksplit:
+        # rank owns columns [k0, k1) of every row; partial Y in fp32, summed by NCCL
+        from paper_2310_06178_b200.sharded import k_split_bounds
+        k0, k1 = k_split_bounds(cfg.k, cfg.d, world, rank)
+        mr, kr = cfg.m, k1 - k0
+        data = np.ascontiguousarray(weights(cfg)[:, k0 // 2:(k1 + 1) // 2])
+        xd = torch.from_numpy(np.ascontiguousarray(Xh[k0:k1])).to(dev)
+        kw = dict(kw, out_dtype=np.float32)
+        y_dt = torch.float32
+    else:
+        if cfg.m % world:
+            raise SystemExit(f"m={cfg.m} not divisible by {world} ranks")
+        mr, kr = cfg.m // world, cfg.k
+        r0 = rank * mr
+        k0, k1 = 0, cfg.k
+        data = weights(cfg)[r0:r0 + mr]
+        xd = torch.from_numpy(Xh).to(dev)
+        y_dt = torch.float32 if exact else xd.dtype
 
     # distinct weight copies so consecutive steps never hit in L2
     shard_bytes = data.nbytes
@@ -239,10 +253,16 @@ def main():
     pwms = []
     for c in range(ncopies):
         dd = base if c == 0 else base.clone()
-        pwms.append(mg.PackedWeightMatrix(m=mr, k=cfg.k, width=4, data=dd,
+        pwms.append(mg.PackedWeightMatrix(m=mr, k=kr, width=4, data=dd,
                                           codebook=mg.int4_codebook()))
     Yshard = torch.empty((mr, cfg.b), dtype=y_dt, device=dev)
     Yfull = torch.empty((cfg.m, cfg.b), dtype=y_dt, device=dev) if world > 1 else Yshard
+
+    def collective():
+        if ksplit:
+            dist.all_reduce(Yshard, op=dist.ReduceOp.SUM)   # Yshard: this rank's fp32 partial
+        else:
+            dist.all_gather_into_tensor(Yfull, Yshard)
     TC = -1  # pseudo-flag: the dequant + tcgen05.mma comparison kernel (K4) instead of msGeMM
     xd16 = xd.half()
     Ytc = torch.empty((mr, cfg.b), dtype=torch.float32, device=dev)
@@ -253,7 +273,7 @@ def main():
             return
         mg.msgemm(pwms[i % ncopies], xd, cfg.d, out=Yshard, _flags=flags | EXTRA_FLAGS, **kw)
         if world > 1 and not flags and gather:
-            dist.all_gather_into_tensor(Yfull, Yshard)
+            collective()
 
     def barrier():
         if world > 1:
@@ -297,7 +317,7 @@ def main():
             for i in range(nsteps):
                 gs[i % ncopies].replay()
                 if flags == 0:
-                    dist.all_gather_into_tensor(Yfull, Yshard)
+                    collective()
             e1.record()
         else:
             e0.record()
@@ -345,10 +365,15 @@ def main():
     def e2e_step(i):
         if world == 1:
             mg.msgemm(pwms[i % ncopies], Xpin, cfg.d, out=Ypin, **kw)
+        elif ksplit:
+            x_dev = Xpin[k0:k1].to(dev, non_blocking=True)
+            mg.msgemm(pwms[i % ncopies], x_dev, cfg.d, out=Yshard, **kw)
+            collective()
+            Ypin.copy_(Yshard.to(Ypin.dtype))
         else:
             x_dev = Xpin.to(dev, non_blocking=True)
             mg.msgemm(pwms[i % ncopies], x_dev, cfg.d, out=Yshard, **kw)
-            dist.all_gather_into_tensor(Yfull, Yshard)
+            collective()
             Ypin.copy_(Yfull)
 
     for i in range(3):
@@ -369,7 +394,7 @@ def main():
     ops = effective_ops(cfg)
     value = ops / (ms_step * 1e-3) / 1e9
     peaks = load_peaks()
-    shard_cfg = type(cfg)(cfg.name, mr, cfg.k, cfg.b, cfg.d, cfg.x_dtype, cfg.seed)
+    shard_cfg = type(cfg)(cfg.name, mr, kr, cfg.b, cfg.d, cfg.x_dtype, cfg.seed)
     y_item = 4 if exact else 2
     bytes_launch = algorithmic_bytes(shard_cfg, x_itemsize=2, y_itemsize=y_item)
     achieved = bytes_launch / (ms_lut * 1e-3) / 1e9
@@ -377,7 +402,7 @@ def main():
     tp = ROOT / "profiles" / "traffic.json"
     if tp.exists():
         traffic = json.loads(tp.read_text()).get(f"{cfg.name}@{world}")
-    nb = cfg.k // cfg.d
+    nb = kr // cfg.d
     smem_bytes = (mr * nb + 2048 * nb) * cfg.b * 2          # LUT reads + half-table writes (fp16)
     out = {
         "metric": "effective GOP/s (2*m*k*b/time) and achieved HBM GB/s vs roofline",
@@ -388,22 +413,25 @@ def main():
         "config": {"workload": cfg.name, "m": cfg.m, "k": cfg.k, "b": cfg.b, "d": cfg.d,
                    "x": "fp16", "tables": "fp16 sign-symmetric half tables (2048/group)",
                    "accum": "f32", "y": "fp32" if exact else "fp16",
-                   "parallelism": f"row-shard x{world}" + (" + NCCL all-gather" if world > 1 else ""),
+                   "parallelism": (f"k-split x{world} + NCCL fp32 all-reduce" if ksplit else
+                                   f"row-shard x{world}" + (" + NCCL all-gather" if world > 1 else "")),
                    "timing": "CUDA-graph replay of the K steps" if use_graphs else "eager launches",
                    "l2": f"rotate {ncopies} weight copies ({ncopies * shard_bytes / 2**20:.0f} MiB "
                          f">= 3x L2) between steps"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
                      "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-                     "kernel": "fused_lut_kernel", "kernel_ms": ms_lut,
+                     "kernel": ("lane_lut_kernel" if (cfg.b == 1 and cfg.d == 3 and not exact)
+                                else "fused_lut_kernel"), "kernel_ms": ms_lut,
                      "kernel_share": ms_lut / ms_step, "algorithmic_bytes_per_launch": bytes_launch,
                      "peak_source": peaks["source"],
                      "smem_lut_bytes_per_launch": smem_bytes,
                      "smem_lut_tbs": smem_bytes / (ms_lut * 1e-3) / 1e12},
         "e2e": {"value": ops / (e2e_ms * 1e-3) / 1e9, "unit": "GOP/s",
-                "ms_per_step": e2e_ms, "h2d_bytes_per_step": Xh.nbytes,
+                "ms_per_step": e2e_ms, "h2d_bytes_per_step": Xh[k0:k1].nbytes,
                 "d2h_bytes_per_step": cfg.m * cfg.b * y_item,
                 "path": "msgemm(pwm, pinned host X) -> host Y" if world == 1 else
-                        "H2D X, msgemm shard, NCCL all-gather, D2H Y"},
+                        ("H2D X slice, msgemm k-slice, NCCL all-reduce, D2H Y" if ksplit else
+                         "H2D X, msgemm shard, NCCL all-gather, D2H Y")},
         "tensor_core_baseline": None if ms_tc is None else {
             "kernel": "K4: int4->fp16 dequant + tcgen05.mma kind::f16, fp32 TMEM accumulation",
             "ms_per_step": ms_tc, "value": effective_ops(shard_cfg) / (ms_tc * 1e-3) / 1e9,

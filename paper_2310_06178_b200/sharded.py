@@ -17,6 +17,7 @@ bit-exact for integer-valued X).
 
 from __future__ import annotations
 
+import math
 from typing import Callable
 
 import numpy as np
@@ -86,3 +87,107 @@ def msgemm_sharded(pwm_local: PackedWeightMatrix, X, d: int, m_total: int, group
     if not isinstance(y, torch.Tensor):
         y = torch.from_numpy(np.ascontiguousarray(y))
     return gather_rows(y, m_total, group)
+
+
+# ----------------------------------------------------------------------------
+# k-split: every rank owns a slice of the inner
+# dimension for ALL rows, so the table build is split too (the replicated
+# build is the Amdahl term of row sharding, §8(e)); the exchange is an fp32
+# sum of the partial Y (all-reduce, or reduce-scatter when the consumer wants
+# row shards).
+# ----------------------------------------------------------------------------
+def k_split_bounds(k: int, d: int, world: int, rank: int, group_size: int = 0) -> tuple[int, int]:
+    """Columns [lo, hi) of rank `rank`'s k-slice.
+
+    Boundaries fall on multiples of lcm(2, d, group_size): whole bytes of the
+    packed rows (packing.py:99-114), whole d-groups (so the slices' lookup
+    blocks are exactly the global blocks, gemm.py:116-133) and whole scale
+    groups.  The last rank also takes the remainder, which holds the global
+    k % d tail (gemm.py:81-83), so the slices' results sum to the full Y.
+    """
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of {world}")
+    if d < 1:
+        raise ValueError("depth d must be >= 1")
+    a = math.lcm(2, d, group_size or 1)
+    base, extra = divmod(k // a, world)
+    lo = (rank * base + min(rank, extra)) * a
+    hi = lo + (base + (1 if rank < extra else 0)) * a
+    return lo, (k if rank == world - 1 else hi)
+
+
+def shard_cols(pwm: PackedWeightMatrix, d: int, world: int, rank: int) -> tuple[PackedWeightMatrix, int, int]:
+    """This rank's k-slice of W as a PackedWeightMatrix, with its bounds.
+
+    The packed payload is sliced on byte boundaries (lo is even); per-row
+    scales are kept (scaling is linear, so each slice may apply them), per-group
+    scales are sliced by column group.
+    """
+    gs = pwm.scales.group_size if isinstance(pwm.scales, PerGroup) else 0
+    lo, hi = k_split_bounds(pwm.k, d, world, rank, gs)
+    data = pwm.data[:, lo // 2:(hi + 1) // 2]
+    scales = pwm.scales
+    if isinstance(scales, PerGroup):
+        scales = PerGroup(group_size=gs, q=scales.q[:, lo // gs:hi // gs])
+    return (PackedWeightMatrix(m=pwm.m, k=hi - lo, width=pwm.width, data=data,
+                               codebook=pwm.codebook, scales=scales), lo, hi)
+
+
+def msgemm_ksplit(pwm_slice: PackedWeightMatrix, X, d: int, lo: int, hi: int, group=None,
+                  local_fn: Callable | None = None, reduce: str = "all"):
+    """Y = W @ X for a k-split W: this rank's partial product over columns
+    [lo, hi) in fp32 (int64 for integer X), then one sum across ranks.
+
+    reduce="all": every rank gets the full (m, b) Y (all-reduce).
+    reduce="scatter": rank r gets rows shard_bounds(m, world, r) (reduce-scatter).
+    The result has X's dtype (reference semantics, gemm.py:113, 153).  X is the
+    full (k, b) activation matrix (replicated); `local_fn(pwm, Xs, d)` must
+    return the partial in its accumulation dtype (default: msgemm with fp32
+    output; the CPU tests substitute the oracle).
+    """
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    Xt = X if isinstance(X, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(X))
+    vec = Xt.dim() == 1
+    X2 = Xt[:, None] if vec else Xt
+    out_dtype = X2.dtype
+    exact = not X2.is_floating_point()
+    acc_dtype = torch.int64 if exact else torch.float32
+    m, b = pwm_slice.m, X2.shape[1]
+    if hi > lo:
+        if local_fn is None:
+            from .gemm import msgemm
+
+            y = msgemm(pwm_slice, X2[lo:hi], d, out_dtype=None if exact else np.float32)
+        else:
+            y = local_fn(pwm_slice, X2[lo:hi], d)
+        y = y if isinstance(y, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(y))
+        y = y.to(acc_dtype).reshape(m, b)
+    else:
+        y = torch.zeros((m, b), dtype=acc_dtype, device=X2.device)
+    if reduce == "all":
+        dist.all_reduce(y, op=dist.ReduceOp.SUM, group=group)
+        out = y.to(out_dtype)
+        return out[:, 0] if vec else out
+    if reduce != "scatter":
+        raise ValueError(f"reduce must be 'all' or 'scatter', got {reduce!r}")
+    spans = [shard_bounds(m, world, r) for r in range(world)]
+    hmax = max(h - l for l, h in spans)
+    if dist.get_backend(group) == "gloo":  # gloo has no reduce-scatter: sum, then slice
+        dist.all_reduce(y, op=dist.ReduceOp.SUM, group=group)
+        part = y[spans[rank][0]:spans[rank][1]]
+    elif all(h - l == hmax for l, h in spans):
+        part = torch.empty((hmax, b), dtype=acc_dtype, device=y.device)
+        dist.reduce_scatter_tensor(part, y.contiguous(), op=dist.ReduceOp.SUM, group=group)
+    else:  # unequal row shards: pad every shard to hmax rows
+        pad = torch.zeros((hmax * world, b), dtype=acc_dtype, device=y.device)
+        for r, (l, h) in enumerate(spans):
+            pad[r * hmax: r * hmax + (h - l)] = y[l:h]
+        part = torch.empty((hmax, b), dtype=acc_dtype, device=y.device)
+        dist.reduce_scatter_tensor(part, pad, op=dist.ReduceOp.SUM, group=group)
+        part = part[: spans[rank][1] - spans[rank][0]]
+    out = part.to(out_dtype)
+    return out[:, 0] if vec else out
