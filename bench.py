@@ -349,6 +349,8 @@ def main():
         step(i, _lib.FLAG_LUT_PHASE_ONLY)
     timed(min(args.steps, 16), _lib.FLAG_LUT_PHASE_ONLY)
     ms_lut = timed(args.steps, _lib.FLAG_LUT_PHASE_ONLY)
+    torch.cuda.synchronize()
+    _lib.reset_workspaces()   # LUT-only launches of the b=1 kernel leave their sums behind
     # the dense tensor-core baseline on the same shard (context, not the metric)
     ms_tc = None
     if cfg.b <= 256:

@@ -68,7 +68,8 @@ extern "C" {
 #define MSG_FLAG_F32_ENTRIES   1  /* fp32 table entries even for fp16 X (exact-int mode)  */
 #define MSG_FLAG_NO_SYMMETRY   2  /* full 16^d tables (default: sign-symmetric half tables) */
 #define MSG_FLAG_FORCE_GENERIC 4  /* global-memory table path (any d, width, dtype)        */
-#define MSG_FLAG_LUT_PHASE_ONLY 8 /* measurement: launch only the fused LUT kernel (Y untouched) */
+#define MSG_FLAG_LUT_PHASE_ONLY 8 /* measurement: launch only the fused LUT kernel (Y untouched;
+                                     a LANE workspace keeps the sums and must be re-zeroed) */
 #define MSG_FLAG_NO_LANE      16  /* do not use the b=1 lane kernel (use the row-block kernel) */
 #define MSG_FLAG_PAIR         32  /* opt-in: double-buffered 2-group row-block kernel (slower on B200, kept for study) */
 #define MSG_FLAG_STATIC_WEIGHTS 64 /* the repacked weights were not written by the kernel launched just
@@ -82,8 +83,9 @@ extern "C" {
 #define MSG_LAYOUT_PAIR 3  /* quad planes, half-quad pair rotation (double-buffered kernel) */
 
 MSG_API const char* msg_last_error(void);
-/* diagnostics: per-CTA trace records {smid, t_start_ns, t_end_ns, units} of
- * the LUT kernels launched while tracing is on (at most 4096, last launch) */
+/* diagnostics: per-CTA trace records {smid, t_start_ns, t_end_ns, units,
+ * phase[4]} (8 x uint64 each) of the LUT kernels launched while tracing is on
+ * (at most 4096, last launch) */
 MSG_API int msg_set_tracing(int on);
 MSG_API int msg_read_trace(uint64_t* host_records, int max_records);
 MSG_API int msg_version(void);
@@ -131,7 +133,10 @@ MSG_API int msg_repack(const uint8_t* packed, int64_t m, int64_t k, int d, int l
 /* ---------- K1+K2: msGeMM (gemm.py:89-153) ---------- */
 
 /* Which layout msg_gemm needs for these arguments (MSG_LAYOUT_*), and the
- * workspace it needs; returns <0 on argument error. */
+ * workspace it needs; returns <0 on argument error.  For MSG_LAYOUT_LANE the
+ * workspace holds the kernel's int64 row sums and tile counters: it must be
+ * zero-filled before its first use and dedicated to LANE calls on one stream
+ * (every call leaves it zero again). */
 MSG_API int msg_gemm_plan(int64_t m, int64_t k, int width, const double* values, int x_dtype,
                   int64_t b, int d, int scale_mode, int64_t group_size, int flags,
                   int* layout_out, int* symmetric_out, int64_t* workspace_bytes_out);

@@ -192,10 +192,13 @@ def to_device(x, dev, non_blocking: bool = False):
 _ws = {}
 
 
-def workspace(nbytes: int, dev):
-    """Per-(device, stream) scratch buffer, grown on demand, never freed on the hot path."""
+def workspace(nbytes: int, dev, kind: str = "scratch"):
+    """Per-(device, stream, kind) scratch buffer, grown on demand, never freed on
+    the hot path.  kind "lane": the b=1 kernel's self-cleaning accumulators
+    (zero-filled here, left zero by every call), kept apart from the scratch
+    the other kernels overwrite."""
     t = torch()
-    key = (dev.index, t.cuda.current_stream(dev).cuda_stream)
+    key = (dev.index, t.cuda.current_stream(dev).cuda_stream, kind)
     buf = _ws.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = t.zeros(max(int(nbytes), 256), dtype=t.uint8, device=dev)
@@ -203,11 +206,19 @@ def workspace(nbytes: int, dev):
     return buf
 
 
+def reset_workspaces():
+    """Zero the self-cleaning "lane" workspaces (needed only after LUT-phase-only
+    measurement launches, which leave their row sums behind)."""
+    for key, buf in _ws.items():
+        if key[2] == "lane":
+            buf.zero_()
+
+
 def read_trace(max_records: int = 4096):
-    """Per-CTA trace records (smid, t0_ns, t1_ns, units) of the last traced launch."""
-    buf = (ctypes.c_uint64 * (4 * max_records))()
+    """Per-CTA trace records (smid, t0_ns, t1_ns, units, phase0..3) of the last traced launch."""
+    buf = (ctypes.c_uint64 * (8 * max_records))()
     n = lib().msg_read_trace(buf, max_records)
     if n < 0:
         check(n)
-    a = np.frombuffer(buf, dtype=np.uint64).reshape(max_records, 4)[:n]
+    a = np.frombuffer(buf, dtype=np.uint64).reshape(max_records, 8)[:n]
     return a[a[:, 2] > 0]

@@ -59,8 +59,14 @@ def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = Fals
     cc = nvcc()
     extra = ["-Xptxas", "-v"] if ptxas_verbose else []
 
+    shared = [p for p in list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h")) + [Path(__file__)]]
+    newest_shared = max(p.stat().st_mtime for p in shared)
+
     def compile_one(src: Path) -> Path:
         obj = objdir / (src.stem + ".o")
+        if (not force and not ptxas_verbose and obj.exists()
+                and obj.stat().st_mtime > max(src.stat().st_mtime, newest_shared)):
+            return obj  # up to date: only changed sources are recompiled
         cmd = [cc, *NVCC_FLAGS, *extra, "-dc" if False else "-c", str(src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), flush=True)

@@ -42,14 +42,14 @@ int run_generic(const uint8_t* packed, int64_t m, int64_t k, int width, const Co
                 cudaStream_t s);
 int64_t generic_workspace_bytes(int64_t m, int64_t k, int width, int x_dtype, int64_t b, int d);
 // b = 1 GEMV kernel (msg_lane.cu)
-bool lane_eligible(int width, int x_dtype, int64_t b, int d, int scale_mode, bool sym,
-                   bool f32_entries);
+bool lane_eligible(int width, const double* values, double beta, int64_t k, int x_dtype,
+                   int64_t b, int d, int scale_mode, bool sym, bool f32_entries);
 int64_t lane_layout_bytes(int64_t m, int64_t k);
-int64_t lane_tail_offset(int64_t m, int64_t k);
-int64_t lane_partial_slices(int64_t m, int64_t k);
+int64_t lane_workspace_bytes(int64_t m, int64_t k);
 int lane_repack(const uint8_t* packed, int64_t m, int64_t k, uint8_t* out, cudaStream_t s);
 int launch_lane(const uint8_t* wrep, int64_t m, int64_t k, const double* values, double beta,
-                const void* x, int x_dtype, float* partial, bool early, cudaStream_t s);
+                const void* x, int scale_mode, const void* q, int q_dtype, void* y, int y_dtype,
+                void* ws, int64_t ws_bytes, bool early, int exp, cudaStream_t s);
 
 static inline int64_t align256(int64_t v) { return (v + 255) / 256 * 256; }
 
@@ -852,10 +852,12 @@ static FusedPlan fused_plan(int64_t m, int64_t k, int width, const double* value
   p.sym = !(flags & MSG_FLAG_NO_SYMMETRY) && codebook_antisymmetric(values, 16, &beta);
   p.f32_entries = (x_dtype == MSG_F32) || (flags & MSG_FLAG_F32_ENTRIES);
   if (!(flags & MSG_FLAG_NO_LANE) &&
-      lane_eligible(width, x_dtype, b, d, scale_mode, p.sym, p.f32_entries)) {
+      lane_eligible(width, values, beta, k, x_dtype, b, d, scale_mode, p.sym, p.f32_entries)) {
+    // one kernel; its workspace (int64 row sums + tile counters) must be zero on
+    // entry and is left zero on exit
     p.lane = true;
-    p.S = (int)lane_partial_slices(m, k);
-    p.partial_bytes = align256((int64_t)p.S * m * 4);
+    p.S = 0;
+    p.partial_bytes = lane_workspace_bytes(m, k);
     p.ok = true;
     return p;
   }
@@ -1042,16 +1044,10 @@ int msg_gemm(const uint8_t* packed, const uint8_t* wrep, int64_t m, int64_t k, i
   if (p.sym) codebook_antisymmetric(values, 16, &beta);
   TailVals tv;
   for (int c = 0; c < 16; ++c) tv.v[c] = (float)values[c];
-  float* partial = reinterpret_cast<float*>(workspace);
-  if (p.lane) {
-    if (int e = launch_lane(wrep, m, k, values, beta, x, x_dtype, partial,
-                                (flags & MSG_FLAG_STATIC_WEIGHTS) != 0, s)) return e;
-    if (flags & MSG_FLAG_LUT_PHASE_ONLY) return MSG_OK;
-    const uint16_t* tailp =
-        (k % 3) ? reinterpret_cast<const uint16_t*>(wrep + lane_tail_offset(m, k)) : nullptr;
-    return launch_finish(partial, p.S, m, 1, k, d, tailp, tv, x, x_dtype, scale_mode, q, q_dtype,
-                         y, y_dtype, s);
-  }
+  if (p.lane)  // LUT_PHASE_ONLY: the LUT kernel alone (its sums stay in the workspace)
+    return launch_lane(wrep, m, k, values, beta, x, scale_mode, q, q_dtype, y, y_dtype,
+                       workspace, ws_bytes, (flags & MSG_FLAG_STATIC_WEIGHTS) != 0,
+                       ((flags >> 16) & 0xFF) | ((flags & MSG_FLAG_LUT_PHASE_ONLY) ? 4 : 0), s);
   FusedParams P{};
   P.wrep = wrep;
   P.lo_off = p.L.lo_off;

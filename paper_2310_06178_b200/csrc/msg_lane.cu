@@ -1,9 +1,9 @@
-// msGeMM GEMV kernel (b = 1, d = 3, fp16 sign-symmetric tables): bank-private
-// tables and a lane-rotated weight layout.
+// msGeMM GEMV kernel (b = 1, d = 3, fp16 X, sign-symmetric fp16 tables):
+// bank-private tables, a lane-rotated weight layout and an in-kernel,
+// deterministic cross-CTA reduction.
 //
 // Reference semantics as in msg_fused.cu (gemm.py:70-153, lut.py:59-72,
-// packing.py:201-228); results go through the same deterministic finish
-// kernel.
+// packing.py:201-228).
 //
 // Why a separate kernel: at b = 1 every table lookup returns 2 bytes, so the
 // gather is bound by instruction issue and shared-memory bank conflicts,
@@ -16,15 +16,20 @@
 //     single wavefront, and each lane accumulates its own row (no cross-lane
 //     reduction);
 //   * K3 stores each row's 32 indices in that rotated order, split into a
-//     10-bit "row" stream (one funnel shift + one LOP3 gives the table byte
-//     offset) and a 2-bit stream (half select, sign), 12 bits per group as in
-//     the reference layout; a warp reads a 32-row tile as three coalesced
-//     512-byte requests;
-//   * accumulation is FHFMA (fp32 += fp16 * +-1, one instruction).
+//     10-bit "row" stream and a 2-bit stream (half select, sign), 12 bits per
+//     group as in the reference layout; a warp reads a 32-row tile as three
+//     coalesced 512-byte requests;
+//   * the byte address is shift + two LOP3s (table base = LDS immediate) and
+//     accumulation is FHFMA (fp32 += fp16 * +-1, one instruction);
+//   * chunk sums meet in int64 fixed point (red.global.add.u64, exact and
+//     order-independent), and the last chunk to reach a 32-row tile writes
+//     its Y -- one kernel per msGeMM, no partial buffer, bitwise
+//     deterministic.
 // Work is the (chunk, row tile) grid linearised chunk-major and split evenly
 // over one persistent CTA per SM, so each table is built by at most two CTAs
 // more than the minimum.
 #include <algorithm>
+#include <cmath>
 
 #include "msg_common.cuh"
 
@@ -103,10 +108,6 @@ __global__ void repack_lane_kernel(const uint8_t* __restrict__ packed, int64_t m
   }
 }
 
-__device__ __forceinline__ void fhfma_l(float& acc, unsigned short h, unsigned short s16) {
-  asm("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(acc) : "h"(h), "h"(s16));
-}
-
 __device__ __forceinline__ uint32_t mul_hi_u32(uint32_t a, uint32_t b) {
   uint32_t r;
   asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
@@ -122,31 +123,38 @@ __device__ __forceinline__ uint32_t funnel_r(uint32_t lo, uint32_t hi) {
 
 struct LaneParams {
   const uint8_t* body;
-  int64_t m, nb, nchunk, ntiles;
-  const void* x;  // (k,) fp16 or fp32
-  float s[16];    // v[c] - beta
+  const uint16_t* tailp;  // (m,) tail codes when k % 3 != 0, else nullptr
+  int64_t m, nb;
+  int nchunk, ntiles, tail;
+  const __half* x;        // (k,) fp16
+  float s[16];            // v[c] - beta
+  float v[16];            // codebook values (tail columns)
   float beta;
-  float* partial;  // [nchunk][m]
+  float fx_scale, fx_inv;  // 2^F, 2^-F: fixed-point grid of the cross-CTA reduction
+  unsigned long long* acc;  // [m] int64 fixed-point row sums (zero between calls)
+  const void* q;
+  int q_dtype, scale_mode;
+  void* y;
+  int y_dtype;
   TraceRec* trace;  // per-CTA trace records or nullptr
   uint32_t ones;    // 0x3C003C00: two fp16 +1.0
   int early;        // MSG_FLAG_STATIC_WEIGHTS: stream weights before griddepcontrol.wait
+  int exp;          // 4: LUT kernel only (measurement); other bits: experiments
 };
 
 constexpr int kLaneThreads = 512;
+constexpr uint32_t kSmemBase = 1024;  // shared-window offset of dynamic smem (no static smem)
 
-__device__ __forceinline__ float to_f(float v) { return v; }
-__device__ __forceinline__ float to_f(__half v) { return __half2float(v); }
-
-// One lookup at position T: the 10-bit row field lands at byte-offset bits
-// 7..16 via one funnel shift, the half select at bit 1, the bank offset
-// (T ^ lane) * 4 at bits 2..6; the fp16 entry is accumulated with FHFMA.
+// One lookup at position T.  The 10-bit row field lands at byte-offset bits
+// 7..16 via one shift, the half select at bit 1, the bank offset (T ^ lane)*4
+// at bits 2..6 (xt); the three do not overlap, so the address is two LOP3s
+// and the table base is the LDS immediate.  The fp16 entry is accumulated
+// with FHFMA (fp32 += fp16 * +-1).
 template <int T>
 __device__ __forceinline__ void lookup(const uint32_t (&w)[12], uint32_t xt, uint32_t S,
                                        float& acc) {
-  // The row field occupies stream bits [10T, 10T+10) and must land at bits
-  // 7..16.  Shifts that stay inside one word use the FMA pipe (IMAD.SHL /
-  // IMAD.HI as >>) so the ALU pipe -- the bound of this kernel -- only does the
-  // masking and the final 3-input add.
+  // Shifts that stay inside one word use the FMA pipe (IMAD.SHL / IMAD.HI as
+  // >>) so the ALU pipe only does the two LOP3s.
   constexpr int S0 = (10 * T) & 31, K = (10 * T) >> 5;
   uint32_t d;
   if constexpr (S0 + 10 <= 32) {
@@ -161,215 +169,299 @@ __device__ __forceinline__ void lookup(const uint32_t (&w)[12], uint32_t xt, uin
   if constexpr (T == 0) hb = w[11] << 1;
   else if constexpr (T == 1) hb = w[11];
   else hb = mul_hi_u32(w[11], 1u << (33 - T));  // == w[11] >> (T - 1)
-  // xt already holds table base + bank offset; the three fields do not overlap
+  // two LOP3s (a & imm) | c, opaque to the compiler so it keeps xt (shared by
+  // the TPW tiles of a step) in a register instead of re-deriving it per lookup
   uint32_t addr;
-  asm("add.u32 %0, %1, %2;" : "=r"(addr) : "r"(d & 0x1FF80u), "r"(hb & 2u));
-  addr += xt;
+  asm("lop3.b32 %0, %1, 0x1FF80, %2, 0xEA;" : "=r"(addr) : "r"(d), "r"(xt));
+  asm("lop3.b32 %0, %1, 2, %0, 0xEA;" : "+r"(addr) : "r"(hb));
   // gather one fp16 entry and accumulate +-entry into fp32; the multiplier is
   // the low (even T) or high (odd T) half of S
   if constexpr (T & 1)
     asm volatile(
         "{\n\t.reg .b16 h, lo, hi;\n\t"
-        "ld.shared.u16 h, [%1];\n\t"
+        "ld.shared.u16 h, [%1+1024];\n\t"
         "mov.b32 {lo, hi}, %2;\n\t"
         "fma.rn.f32.f16 %0, h, hi, %0;\n\t}"
         : "+f"(acc) : "r"(addr), "r"(S));
   else
     asm volatile(
         "{\n\t.reg .b16 h, lo, hi;\n\t"
-        "ld.shared.u16 h, [%1];\n\t"
+        "ld.shared.u16 h, [%1+1024];\n\t"
         "mov.b32 {lo, hi}, %2;\n\t"
         "fma.rn.f32.f16 %0, h, lo, %0;\n\t}"
         : "+f"(acc) : "r"(addr), "r"(S));
 }
 
 template <int T, int TPW>
-__device__ __forceinline__ void steps(const uint32_t (&w)[TPW][12], uint32_t tab,
-                                      uint32_t lane4, uint32_t ones, float (&acc)[TPW]) {
+__device__ __forceinline__ void steps(const uint32_t (&w)[TPW][12], uint32_t lane4,
+                                      uint32_t ones, float (&acc)[TPW][2]) {
   if constexpr (T < 32) {
-    const uint32_t xt = tab + (lane4 ^ (uint32_t)(T << 2));  // base + bank of group T ^ lane
+    const uint32_t xt = lane4 ^ (uint32_t)(T << 2);  // bank of group T ^ lane
 #pragma unroll
     for (int u = 0; u < TPW; ++u) {
       // +-1.0h multipliers of positions 2q, 2q+1 (sign bits at 15-q, 31-q)
       const uint32_t S = ((w[u][10] << (T >> 1)) & 0x80008000u) | ones;
-      lookup<T>(w[u], xt, S, acc[u]);
+      lookup<T>(w[u], xt, S, acc[u][T & 1]);
     }
-    steps<T + 1, TPW>(w, tab, lane4, ones, acc);
+    steps<T + 1, TPW>(w, lane4, ones, acc);
   }
+}
+
+__device__ __forceinline__ void red_add_u64(unsigned long long* p, long long v) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 constexpr int kTableBytes = 128 * 1024;
 constexpr int kTileBytes = 1536;             // one 32-row tile of one chunk
-constexpr int kRing = 4;                     // tiles in flight per warp (TMA ring)
+constexpr int kRing = 4;                     // tiles in flight per warp (TMA ring of batches)
 constexpr int kNW = kLaneThreads / 32;
-constexpr int kLaneSmem = kTableBytes + kNW * kRing * kTileBytes + kNW * kRing * 8;
+constexpr int kLaneSmem = kTableBytes + kNW * kRing * kTileBytes + kNW * kRing * 8 + 16;
 
-// Work unit = "superbatch": TPW*kNW consecutive row tiles of one chunk, so that
-// every warp gets exactly one batch of TPW tiles per superbatch; superbatches
-// (chunk-major) are split evenly over one CTA per SM.  Each warp streams its
-// tiles through a kRing-deep ring of shared-memory slots filled by
-// cp.async.bulk (lane 0 issues, one mbarrier per slot), so the weight stream
-// has kNW*kRing*1.5 KB in flight per SM independently of the table build.
-template <typename XT, int TPW>
+// Y from the fixed-point row sums: k % 3 tail, per-row scale, Y's dtype
+// (gemm.py:70-86).  Launched with PDL behind the LUT kernel: operands that do
+// not depend on it (tail codes and activations, scales) are loaded before
+// griddepcontrol.wait, which returns once every red of the LUT kernel is
+// visible.  Each thread owns two rows (16 B of sums, read through L2 and
+// cleared for the next call).
+__global__ void __launch_bounds__(256) lane_finish_kernel(LaneParams P) {
+  const int64_t row = ((int64_t)blockIdx.x * 256 + threadIdx.x) * 2;
+  const bool live = row < P.m;
+  float add0 = 0.f, add1 = 0.f, q0 = 1.f, q1 = 1.f;
+  if (live) {
+    if (P.tail) {
+      const uint32_t tc = *reinterpret_cast<const uint32_t*>(P.tailp + row);  // rows row, row+1
+      for (int u = 0; u < P.tail; ++u) {
+        const float xv = __half2float(P.x[P.nb * 3 + u]);
+        add0 = fmaf(P.v[(tc >> (4 * u)) & 0xF], xv, add0);
+        add1 = fmaf(P.v[(tc >> (16 + 4 * u)) & 0xF], xv, add1);
+      }
+    }
+    if (P.scale_mode == MSG_SCALE_PER_ROW) {
+      q0 = load_as<float>(P.q, P.q_dtype, row);
+      if (row + 1 < P.m) q1 = load_as<float>(P.q, P.q_dtype, row + 1);
+    }
+  }
+  griddep_wait();
+  griddep_launch_dependents();
+  if (!live) return;
+  ulonglong2* ap = reinterpret_cast<ulonglong2*>(P.acc + row);
+  const ulonglong2 raw = __ldcg(ap);
+  __stcg(ap, make_ulonglong2(0ull, 0ull));
+  // the tail is added to the rounded fp32 sum, as the reference adds it to
+  // the block sum (gemm.py:81-83)
+  float y0 = __ll2float_rn((long long)raw.x) * P.fx_inv;
+  y0 = (y0 + add0) * q0;
+  store_as<float>(P.y, P.y_dtype, row, y0);
+  if (row + 1 < P.m) {
+    float y1 = __ll2float_rn((long long)raw.y) * P.fx_inv;
+    y1 = (y1 + add1) * q1;
+    store_as<float>(P.y, P.y_dtype, row + 1, y1);
+  }
+}
+
+// Work split: the (chunk, 32-row tile) grid linearised chunk-major,
+// g = chunk * ntiles + tile -- which is also the order of the tiles in HBM --
+// is cut into one contiguous range per CTA (one CTA per SM).  A range covers
+// one or two chunks ("segments"); per segment the CTA builds the chunk's
+// tables once and warp w takes a contiguous run of the segment, TPW tiles per batch.  Each warp streams its
+// batches through a ring of kRing/TPW shared-memory slots, one cp.async.bulk
+// and one mbarrier per batch (lane 0 issues), so the weight stream keeps
+// kNW*kRing*1.5 KB in flight per SM through the table builds.
+//
+// Cross-CTA reduction (no partial buffer, no second kernel): every lane rounds
+// its row's chunk sum onto the fixed-point grid 2^-F and adds it with one
+// 64-bit integer red into acc[row]; integer addition is associative, so Y is
+// bitwise deterministic whatever the arrival order.  lane_finish_kernel,
+// launched behind it with PDL, turns the sums into Y.
+template <int TPW>
 __global__ void __launch_bounds__(kLaneThreads, 1) lane_lut_kernel(LaneParams P) {
-  extern __shared__ __align__(128) uint8_t smem[];  // table | rings | mbarriers
-  constexpr int SB = TPW * kNW;                     // tiles per superbatch
+  extern __shared__ __align__(1024) uint8_t smem[];  // table | rings | mbarriers | scratch
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int kSlots = kRing / TPW;                // ring slots of one batch each
   uint8_t* ring = smem + kTableBytes + warp * kRing * kTileBytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kTableBytes + kNW * kRing * kTileBytes) +
                    warp * kRing;
-  const int64_t nsb = (P.ntiles + SB - 1) / SB;  // superbatches per chunk
-  const int64_t U = P.nchunk * nsb;
-  const int64_t u_begin = U * blockIdx.x / gridDim.x;
-  const int64_t u_end = U * (blockIdx.x + 1) / gridDim.x;
-  __shared__ float corr_s;
+  float* corr_s = reinterpret_cast<float*>(smem + kTableBytes + kNW * kRing * kTileBytes +
+                                           kNW * kRing * 8);
+  if (tid == 0 && smem_u32(smem) != kSmemBase) __trap();  // the LDS immediate assumes it
+  const int nt = P.ntiles;
+  const int64_t G = (int64_t)P.nchunk * nt;  // < 2^31 (checked at launch)
+  const int G0 = (int)(G * blockIdx.x / gridDim.x), G1 = (int)(G * (blockIdx.x + 1) / gridDim.x);
   const unsigned long long t_start = P.trace ? global_ns() : 0ull;
+  unsigned long long t_build = 0, t_wait = 0, t_loop = 0, t_count = 0;  // trace phases
 
   if (lane == 0)
-    for (int i = 0; i < kRing; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < kSlots; ++i) mbar_init(&bars[i], 1);
   fence_mbar_init();
   __syncwarp();
 
-  // Issue cursor (lane-uniform, no division on the hot path): chunk nc,
-  // superbatch ns within it, tile nq of this warp's batch; nu = linear unit.
-  // Tile of this warp for (ns, nq) is ns*SB + warp*TPW + nq.
-  uint32_t issued = 0, consumed = 0;  // per-warp ring counters (lane-uniform)
-  int64_t nu = u_begin, nc = u_begin / nsb, ns = u_begin - (u_begin / nsb) * nsb;
-  int nq = 0;
-  // keep kRing tiles of this warp in flight, in consumption order (lane 0 issues)
+  // Warp w's tiles of a segment [sb, se) are the contiguous run
+  // [sb + n w / 16, sb + n (w + 1) / 16), n = se - sb, consumed TPW at a time.
+  // Issue cursor (lane-uniform): next tile gi of the run ending at ge, in the
+  // segment ending at se; gi == G1 when the CTA's range is exhausted.
+  auto run_of = [&](int sb, int se, int& b, int& e) {
+    const int n = se - sb;
+    b = sb + (n * warp) / kNW;
+    e = sb + (n * (warp + 1)) / kNW;
+  };
+  uint32_t issued = 0, consumed = 0;  // per-warp ring counters
+  int gi, ge, se = min(G1, (G0 / nt + 1) * nt);
+  run_of(G0, se, gi, ge);
+  auto next_run = [&]() {  // skip to this warp's run in the following segment(s)
+    while (gi == ge) {
+      if (se >= G1) { gi = ge = G1; return; }
+      const int sb = se;
+      se = min(G1, sb + nt);
+      run_of(sb, se, gi, ge);
+    }
+  };
+  next_run();
+  // one bulk copy per batch: the batch's tiles are contiguous in HBM
   auto refill = [&]() {
-    while (issued - consumed < (uint32_t)kRing && nu < u_end) {
-      const int64_t t = ns * SB + warp * TPW + nq;
-      if (t < P.ntiles) {
-        if (lane == 0) {
-          const int slot = issued % kRing;
-          fence_proxy_async();
-          mbar_expect_tx(&bars[slot], kTileBytes);
-          bulk_g2s(ring + slot * kTileBytes, P.body + (nc * P.ntiles + t) * kTileBytes,
-                   kTileBytes, &bars[slot]);
-        }
-        ++issued;
+    while (issued - consumed < (uint32_t)kSlots && gi < G1) {
+      const int nv = min(TPW, ge - gi);
+      if (lane == 0) {
+        const int slot = issued % kSlots;
+        mbar_expect_tx(&bars[slot], nv * kTileBytes);
+        bulk_g2s(ring + slot * (TPW * kTileBytes), P.body + (int64_t)gi * kTileBytes,
+                 nv * kTileBytes, &bars[slot]);
       }
-      if (++nq == TPW) {
-        nq = 0;
-        ++nu;
-        if (++ns == nsb) { ns = 0; ++nc; }
-      }
+      ++issued;
+      gi += nv;
+      if (gi == ge) next_run();
     }
   };
 
-  // activations are prefetched as raw XT values and converted at the build,
-  // so the load latency is not exposed where the prefetch is issued
-  auto load_x = [&](int64_t c, XT& x0, XT& x1, XT& x2) {
-    x0 = x1 = x2 = XT(0.f);
+  // activations are prefetched as raw fp16 and converted at the build
+  auto load_x = [&](int c, __half& x0, __half& x1, __half& x2) {
+    x0 = x1 = x2 = __float2half(0.f);
     const int64_t g = c * 32 + lane;
     if (c < P.nchunk && g < P.nb) {
-      const XT* xp = reinterpret_cast<const XT*>(P.x) + 3 * g;
+      const __half* xp = P.x + 3 * g;
       x0 = xp[0];
       x1 = xp[1];
       x2 = xp[2];
     }
   };
-  XT xn0, xn1, xn2;
+  __half xn0, xn1, xn2;
   // Launched with PDL: the prologue overlaps the previous kernel's tail.  The
   // weight stream may start before the wait only if the previous kernel did
-  // not write it; x and the partials are touched only after the wait.
+  // not write it; x and acc are touched only after the wait.
   if (P.early) refill();
   griddep_wait();
-  griddep_launch_dependents();  // the finish kernel may queue behind this grid
+  griddep_launch_dependents();
   if (!P.early) refill();
-  load_x(u_begin / nsb, xn0, xn1, xn2);
+  load_x(G0 / nt, xn0, xn1, xn2);
 
-  int64_t u = u_begin;
-  while (u < u_end) {
-    const int64_t c = u / nsb;
-    const int64_t sb_end = std::min<int64_t>(u_end, (c + 1) * nsb);  // this chunk's share
-    const float x0 = to_f(xn0), x1 = to_f(xn1), x2 = to_f(xn2);
+  const uint32_t lane4 = (uint32_t)lane << 2;
+  const uint32_t ones = P.ones;  // 0x3C003C00 from the parameter block (one LOP3 for S)
+  for (int seg_b = G0; seg_b < G1;) {
+    const int c = seg_b / nt;
+    const int seg_e = min(G1, (c + 1) * nt);
+    const float x0 = __half2float(xn0), x1 = __half2float(xn1), x2 = __half2float(xn2);
     load_x(c + 1, xn0, xn1, xn2);  // prefetch the next chunk's activations
     // ---- build chunk c's 32 bank-private half tables (groups beyond nb get
     // x = 0, i.e. all-zero tables, so padded positions contribute nothing)
     __syncthreads();
+    const unsigned long long tb0 = P.trace ? global_ns() : 0ull;
     {
-      const int j = lane;
-      float a[16];
-#pragma unroll
-      for (int v = 0; v < 16; ++v) a[v] = P.s[v] * x0;
       if (warp == 0) {
         float sx = x0 + x1 + x2;
 #pragma unroll
         for (int o = 16; o >= 1; o >>= 1) sx += __shfl_xor_sync(0xffffffffu, sx, o);
-        if (lane == 0) corr_s = P.beta * sx;
+        if (lane == 0) *corr_s = P.beta * sx;
       }
       // warp w (of 16) builds rows u0 | u1<<4 | u2lo<<8 with u2lo = w/4 and
       // u1 in [4(w%4), 4(w%4)+4); the high half of word (row, j) is entry
-      // row + 1024 (u2 = u2lo + 4)
+      // row + 1024 (u2 = u2lo + 4).  fp16 entry = (s[u0] x0) + (s[u1] x1 +
+      // s[u2] x2): both terms rounded to fp16, one HADD2 per word.
       static_assert(kLaneThreads == 512, "build split assumes 16 warps");
+      __half2 a2[16];
+#pragma unroll
+      for (int v = 0; v < 16; ++v) a2[v] = __float2half2_rn(P.s[v] * x0);
       const int u2lo = warp >> 2;
       const float c0 = P.s[u2lo] * x2, c1 = P.s[u2lo + 4] * x2;
-      uint32_t* tw = reinterpret_cast<uint32_t*>(smem);
-#pragma unroll 2
+      __half2* tw = reinterpret_cast<__half2*>(smem);
+#pragma unroll
       for (int hh = 0; hh < 4; ++hh) {
         const int u1 = (warp & 3) * 4 + hh;
         const float bv = P.s[u1] * x1;
-        const float bc0 = bv + c0, bc1 = bv + c1;
-        uint32_t* dst = tw + ((u1 << 4) | (u2lo << 8)) * 32 + j;
+        const __half2 bc = __floats2half2_rn(bv + c0, bv + c1);
+        __half2* dst = tw + ((u1 << 4) | (u2lo << 8)) * 32 + lane;
 #pragma unroll
-        for (int u0 = 0; u0 < 16; ++u0) {
-          __half2 h2 = __floats2half2_rn(a[u0] + bc0, a[u0] + bc1);
-          dst[u0 * 32] = *reinterpret_cast<uint32_t*>(&h2);
-        }
+        for (int u0 = 0; u0 < 16; ++u0) dst[u0 * 32] = __hadd2(a2[u0], bc);
       }
     }
     __syncthreads();
-    const float corr = corr_s;
-    const uint32_t lane4 = (uint32_t)lane << 2;
-    const uint32_t tab32 = smem_u32(smem);
-    const uint32_t ones = P.ones;  // 0x3C003C00 from the parameter block (one LOP3 for S)
-    for (; u < sb_end; ++u) {
-      const int64_t sb = u - c * nsb;
-      const int64_t t0 = sb * SB + warp * TPW;
+    if (P.trace) t_build += global_ns() - tb0;
+    const float corr = *corr_s;
+    int cb, ce;
+    run_of(seg_b, seg_e, cb, ce);
+    for (int b0 = cb; b0 < ce; b0 += TPW) {
+      const int nv = min(TPW, ce - b0);  // tiles of this batch
       uint32_t w[TPW][12];
+      {
+        const int slot = consumed % kSlots;
+        mbar_wait(&bars[slot], (consumed / kSlots) & 1);
+        ++consumed;
+        const uint4* tb = reinterpret_cast<const uint4*>(ring + slot * (TPW * kTileBytes));
 #pragma unroll
-      for (int q = 0; q < TPW; ++q) {
-        if (t0 + q < P.ntiles) {
-          const int slot = consumed % kRing;
-          mbar_wait(&bars[slot], (consumed / kRing) & 1);
-          const uint4* tb = reinterpret_cast<const uint4*>(ring + slot * kTileBytes);
-          uint4 v0 = tb[lane], v1 = tb[32 + lane], v2 = tb[64 + lane];
-          w[q][0] = v0.x; w[q][1] = v0.y; w[q][2] = v0.z; w[q][3] = v0.w;
-          w[q][4] = v1.x; w[q][5] = v1.y; w[q][6] = v1.z; w[q][7] = v1.w;
-          w[q][8] = v2.x; w[q][9] = v2.y; w[q][10] = v2.z; w[q][11] = v2.w;
-          ++consumed;
-        } else {
+        for (int q = 0; q < TPW; ++q) {
+          if (q < nv) {
+            uint4 v0 = tb[q * 96 + lane], v1 = tb[q * 96 + 32 + lane], v2 = tb[q * 96 + 64 + lane];
+            w[q][0] = v0.x; w[q][1] = v0.y; w[q][2] = v0.z; w[q][3] = v0.w;
+            w[q][4] = v1.x; w[q][5] = v1.y; w[q][6] = v1.z; w[q][7] = v1.w;
+            w[q][8] = v2.x; w[q][9] = v2.y; w[q][10] = v2.z; w[q][11] = v2.w;
+          } else {
 #pragma unroll
-          for (int e = 0; e < 12; ++e) w[q][e] = 0;
+            for (int e = 0; e < 12; ++e) w[q][e] = 0;
+          }
         }
       }
       __syncwarp();  // every lane has copied its words out of the consumed slots
       refill();
-      float acc[TPW];
+      float acc[TPW][2];
 #pragma unroll
-      for (int q = 0; q < TPW; ++q) acc[q] = corr;
-      steps<0, TPW>(w, tab32, lane4, ones, acc);
+      for (int q = 0; q < TPW; ++q) { acc[q][0] = corr; acc[q][1] = 0.f; }
+      steps<0, TPW>(w, lane4, ones, acc);
+      const int64_t row0 = (int64_t)(b0 - c * nt) * 32 + lane;
 #pragma unroll
       for (int q = 0; q < TPW; ++q) {
-        const int64_t row = (t0 + q) * 32 + lane;
-        if (t0 + q < P.ntiles && row < P.m) P.partial[c * P.m + row] = acc[q];
+        const int64_t row = row0 + q * 32;
+        const long long fx = __float2ll_rn((acc[q][0] + acc[q][1]) * P.fx_scale);
+        if (q < nv && row < P.m) red_add_u64(P.acc + row, fx);
       }
     }
+    seg_b = seg_e;
   }
+  if (P.trace) t_loop = global_ns();
   if (P.trace) {
     __syncthreads();
     if (tid == 0 && blockIdx.x < kTraceMax)
       P.trace[blockIdx.x] =
-          TraceRec{sm_id(), t_start, global_ns(), (unsigned long long)(u_end - u_begin)};
+          TraceRec{sm_id(), t_start, global_ns(), (unsigned long long)(G1 - G0),
+                   {t_build, t_wait, t_loop, t_count}};
   }
 }
 
-bool lane_eligible(int width, int x_dtype, int64_t b, int d, int scale_mode, bool sym,
-                   bool f32_entries) {
-  return width == 4 && d == 3 && b == 1 && sym && !f32_entries &&
-         (x_dtype == MSG_F16 || x_dtype == MSG_F32) && scale_mode != MSG_SCALE_PER_GROUP;
+// Fixed-point exponent F of the cross-CTA reduction: a chunk sum is bounded by
+// 96 * (max|s| + |beta|) * 65504 (fp16 X), and nchunk of them must fit int64.
+static int lane_fixed_point_exp(const double* values, double beta, int64_t nchunk) {
+  double smax = 0;
+  for (int c = 0; c < 16; ++c) smax = std::max(smax, std::fabs(values[c] - beta));
+  const double bound = 96.0 * (smax + std::fabs(beta)) * 65504.0;
+  const int eb = (int)std::ceil(std::log2(std::max(bound, 1.0))) + 1;
+  const int en = (int)std::ceil(std::log2((double)nchunk + 1.0));
+  return 62 - en - eb;
+}
+
+bool lane_eligible(int width, const double* values, double beta, int64_t k, int x_dtype,
+                   int64_t b, int d, int scale_mode, bool sym, bool f32_entries) {
+  if (!(width == 4 && d == 3 && b == 1 && sym && !f32_entries && x_dtype == MSG_F16 &&
+        scale_mode != MSG_SCALE_PER_GROUP && k >= 3))
+    return false;
+  const int64_t nchunk = (k / 3 + 31) / 32;
+  return nchunk < (1 << 20) && lane_fixed_point_exp(values, beta, nchunk) >= 8;
 }
 
 int lane_repack(const uint8_t* packed, int64_t m, int64_t k, uint8_t* out, cudaStream_t s) {
@@ -382,21 +474,25 @@ int lane_repack(const uint8_t* packed, int64_t m, int64_t k, uint8_t* out, cudaS
   return MSG_OK;
 }
 
-int64_t lane_partial_slices(int64_t m, int64_t k) { return lane_layout(m, k).nchunk; }
+// workspace: [32 * ntiles] int64 accumulators (rows padded to whole tiles),
+// zero on entry and on exit
+int64_t lane_workspace_bytes(int64_t m, int64_t k) {
+  LaneLayout L = lane_layout(m, k);
+  return align256l(L.ntiles * 32 * 8);
+}
 
-template <typename XT, int TPW>
+template <int TPW>
 static int launch_lane_t(const LaneParams& P, cudaStream_t s) {
   static int configured_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (configured_dev != dev) {
-    MSG_CUDA_CHECK(cudaFuncSetAttribute(lane_lut_kernel<XT, TPW>,
+    MSG_CUDA_CHECK(cudaFuncSetAttribute(lane_lut_kernel<TPW>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kLaneSmem));
     configured_dev = dev;
   }
-  const int64_t nsb = (P.ntiles + TPW * kNW - 1) / (TPW * kNW);
-  const int64_t U = P.nchunk * nsb;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(U, sm_count()));
+  const int64_t G = (int64_t)P.nchunk * P.ntiles;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(G, sm_count()));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kLaneThreads);
@@ -407,37 +503,55 @@ static int launch_lane_t(const LaneParams& P, cudaStream_t s) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  MSG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, lane_lut_kernel<XT, TPW>, P));
+  MSG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, lane_lut_kernel<TPW>, P));
+  if (P.exp & 4) return MSG_OK;  // measurement: LUT kernel alone
+  // the finishing kernel, queued with PDL behind the LUT kernel
+  cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, ceil_div((P.m + 1) / 2, 256)));
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  MSG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, lane_finish_kernel, P));
   return MSG_OK;
 }
 
-template <typename XT>
-static int launch_lane_x(const LaneParams& P, cudaStream_t s) {
-  // superbatch granularity: 2 tiles per warp when every SM gets several
-  // superbatches, else 1 (finer split, better balance on small problems)
-  const int64_t sb2 = P.nchunk * ((P.ntiles + 2 * kNW - 1) / (2 * kNW));
-  if (sb2 >= 4 * (int64_t)sm_count()) return launch_lane_t<XT, 2>(P, s);
-  return launch_lane_t<XT, 1>(P, s);
-}
-
 int launch_lane(const uint8_t* wrep, int64_t m, int64_t k, const double* values, double beta,
-                const void* x, int x_dtype, float* partial, bool early, cudaStream_t s) {
+                const void* x, int scale_mode, const void* q, int q_dtype, void* y, int y_dtype,
+                void* ws, int64_t ws_bytes, bool early, int exp, cudaStream_t s) {
   LaneLayout L = lane_layout(m, k);
+  if (ws_bytes < lane_workspace_bytes(m, k))
+    return fail(MSG_ERR_WORKSPACE, "workspace too small: need %lld bytes",
+                (long long)lane_workspace_bytes(m, k));
+  if (L.nchunk * L.ntiles >= (1ll << 31)) return fail(MSG_ERR_UNSUPPORTED, "problem too large");
   LaneParams P{};
   P.body = wrep + L.body_off;
+  P.tailp = L.tail ? reinterpret_cast<const uint16_t*>(wrep + L.tail_off) : nullptr;
   P.m = m;
   P.nb = L.nb;
-  P.nchunk = L.nchunk;
-  P.ntiles = L.ntiles;
-  P.x = x;
-  for (int c = 0; c < 16; ++c) P.s[c] = (float)(values[c] - beta);
+  P.nchunk = (int)L.nchunk;
+  P.ntiles = (int)L.ntiles;
+  P.tail = (int)L.tail;
+  P.x = reinterpret_cast<const __half*>(x);
+  for (int c = 0; c < 16; ++c) {
+    P.s[c] = (float)(values[c] - beta);
+    P.v[c] = (float)values[c];
+  }
   P.beta = (float)beta;
-  P.partial = partial;
+  const int F = lane_fixed_point_exp(values, beta, L.nchunk);
+  P.fx_scale = std::ldexp(1.0f, F);
+  P.fx_inv = std::ldexp(1.0f, -F);
+  P.acc = reinterpret_cast<unsigned long long*>(ws);
+  P.q = q;
+  P.q_dtype = q_dtype;
+  P.scale_mode = scale_mode;
+  P.y = y;
+  P.y_dtype = y_dtype;
   P.trace = trace_buffer();
   P.ones = 0x3C003C00u;
   P.early = early ? 1 : 0;
-  if (x_dtype == MSG_F16) return launch_lane_x<__half>(P, s);
-  return launch_lane_x<float>(P, s);
+  P.exp = exp;
+  // 2 tiles per warp batch (ILP) when every CTA gets at least two batches per
+  // warp, else 1 (finer split, better balance on small problems)
+  if (L.nchunk * L.ntiles >= 4LL * kNW * sm_count()) return launch_lane_t<2>(P, s);
+  return launch_lane_t<1>(P, s);
 }
 
 }  // namespace msg

@@ -170,7 +170,8 @@ def msgemm(pwm: PackedWeightMatrix, X, d: int, budget: int = DEFAULT_BUDGET,
             if pwm.has_device_layout(dev, d, layout.value, sym.value):
                 flags |= _lib.FLAG_STATIC_WEIGHTS
             wrep = pwm.device_layout(dev, d, layout.value, sym.value)
-        ws = _lib.workspace(ws_bytes.value, dev)
+        ws = _lib.workspace(ws_bytes.value, dev,
+                            "lane" if layout.value == _lib.LAYOUT_LANE else "scratch")
         _lib.check(lib.msg_gemm(
             _lib.ptr(pwm.device_data(dev)), _lib.ptr(wrep), m, k, pwm.width, vals,
             _lib.ptr(xd), x_code, b, d, scale_mode, group_size, _lib.ptr(qd), q_code,
