@@ -120,13 +120,19 @@ def torch():
     return _t
 
 
+_dev_ok = False
+
+
 def require_device():
     """The CUDA device this call runs on; raise loudly if there is none."""
+    global _dev_ok
     t = torch()
-    if not t.cuda.is_available():
-        raise RuntimeError("msgemm_b200 needs a CUDA device (B200, sm_100a); "
-                           "there is no CPU fallback")
-    lib()
+    if not _dev_ok:
+        if not t.cuda.is_available():
+            raise RuntimeError("msgemm_b200 needs a CUDA device (B200, sm_100a); "
+                               "there is no CPU fallback")
+        lib()
+        _dev_ok = True
     return t.device("cuda", t.cuda.current_device())
 
 

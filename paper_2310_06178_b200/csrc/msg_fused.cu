@@ -162,6 +162,7 @@ struct FusedParams {
   int64_t b;
   float s[16];  // per-code value used in tables: v[c] - beta (symmetric) or v[c]
   float beta;
+  int s_exact16;        // every s[c] is exact in fp16 (fp16x2 table build allowed)
   int quads_per_slice;  // k-slice length in quads
   int ql;               // quads per table round
   float* partial;       // [S][m][b]
@@ -421,17 +422,43 @@ __global__ void __launch_bounds__(kThreads, 1) fused_lut_kernel(FusedParams P) {
       for (int c = 0; c < BC; ++c) xtop[c] = xt[c];
       uint8_t* dst = tab + (size_t)qq * QUADB;
       const uint32_t gslot_b = (uint32_t)g << 5;
+      if (sizeof(ET) == 2 && BC >= 2 && P.s_exact16) {
+        // fp16 entries: the low-code part and the top-code term rounded to
+        // fp16 once each, then one HFMA2 per column pair (entry = base + s_h x_top)
+        constexpr int NP = BC >= 2 ? BC / 2 : 1;
+        __half2 b2[NP], t2[NP];
 #pragma unroll
-      for (int h = 0; h < HIN; ++h) {
-        float e[BC];
-        if constexpr (BC == 1) {
-          e[0] = fmaf(sv[h], xtop[0], base[0]);
-        } else {
-#pragma unroll
-          for (int c = 0; c < BC; c += 2)
-            fma2_to(e[c], e[c + 1], sv[h], xtop[c], xtop[c + 1], base[c], base[c + 1]);
+        for (int c = 0; c < BC; c += 2) {
+          b2[c / 2] = __floats2half2_rn(base[c], base[c + 1]);
+          t2[c / 2] = __floats2half2_rn(xtop[c], xtop[c + 1]);
         }
-        store_entry<ET, BC>(dst + TL::off((uint32_t)(low + h * LOWN), gslot_b), e);
+#pragma unroll
+        for (int h = 0; h < HIN; ++h) {
+          const __half2 s2 = __float2half2_rn(sv[h]);  // codebook values are exact in fp16
+          uint32_t wv[NP];
+#pragma unroll
+          for (int c = 0; c < BC / 2; ++c) {
+            __half2 e2 = __hfma2(s2, t2[c], b2[c]);
+            wv[c] = *reinterpret_cast<uint32_t*>(&e2);
+          }
+          uint8_t* p = dst + TL::off((uint32_t)(low + h * LOWN), gslot_b);
+          if constexpr (BC == 2) *reinterpret_cast<uint32_t*>(p) = wv[0];
+          else if constexpr (BC == 4) *reinterpret_cast<uint2*>(p) = make_uint2(wv[0], wv[1]);
+          else *reinterpret_cast<uint4*>(p) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        }
+      } else {
+#pragma unroll
+        for (int h = 0; h < HIN; ++h) {
+          float e[BC];
+          if constexpr (BC == 1) {
+            e[0] = fmaf(sv[h], xtop[0], base[0]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BC; c += 2)
+              fma2_to(e[c], e[c + 1], sv[h], xtop[c], xtop[c + 1], base[c], base[c + 1]);
+          }
+          store_entry<ET, BC>(dst + TL::off((uint32_t)(low + h * LOWN), gslot_b), e);
+        }
       }
     }
     __syncthreads();
@@ -1058,7 +1085,11 @@ int msg_gemm(const uint8_t* packed, const uint8_t* wrep, int64_t m, int64_t k, i
   P.nq = p.L.nq;
   P.x = x;
   P.b = b;
-  for (int c = 0; c < 16; ++c) P.s[c] = (float)(values[c] - beta);
+  P.s_exact16 = 1;
+  for (int c = 0; c < 16; ++c) {
+    P.s[c] = (float)(values[c] - beta);
+    if ((double)__half2float(__float2half_rn(P.s[c])) != values[c] - beta) P.s_exact16 = 0;
+  }
   P.beta = (float)beta;
   P.quads_per_slice = p.quads_per_slice;
   P.ql = p.ql;

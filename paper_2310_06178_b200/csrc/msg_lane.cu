@@ -218,45 +218,51 @@ constexpr int kNW = kLaneThreads / 32;
 constexpr int kLaneSmem = kTableBytes + kNW * kRing * kTileBytes + kNW * kRing * 8 + 16;
 
 // Y from the fixed-point row sums: k % 3 tail, per-row scale, Y's dtype
-// (gemm.py:70-86).  Launched with PDL behind the LUT kernel: operands that do
-// not depend on it (tail codes and activations, scales) are loaded before
-// griddepcontrol.wait, which returns once every red of the LUT kernel is
-// visible.  Each thread owns two rows (16 B of sums, read through L2 and
-// cleared for the next call).
-__global__ void __launch_bounds__(256) lane_finish_kernel(LaneParams P) {
-  const int64_t row = ((int64_t)blockIdx.x * 256 + threadIdx.x) * 2;
-  const bool live = row < P.m;
-  float add0 = 0.f, add1 = 0.f, q0 = 1.f, q1 = 1.f;
-  if (live) {
-    if (P.tail) {
-      const uint32_t tc = *reinterpret_cast<const uint32_t*>(P.tailp + row);  // rows row, row+1
-      for (int u = 0; u < P.tail; ++u) {
-        const float xv = __half2float(P.x[P.nb * 3 + u]);
-        add0 = fmaf(P.v[(tc >> (4 * u)) & 0xF], xv, add0);
-        add1 = fmaf(P.v[(tc >> (16 + 4 * u)) & 0xF], xv, add1);
-      }
-    }
-    if (P.scale_mode == MSG_SCALE_PER_ROW) {
-      q0 = load_as<float>(P.q, P.q_dtype, row);
-      if (row + 1 < P.m) q1 = load_as<float>(P.q, P.q_dtype, row + 1);
+// (gemm.py:70-86), two rows (16 B of sums) per thread, in a kernel queued
+// with PDL behind the LUT kernel: operands that do not depend on the sums
+// (tail codes and activations, scales) are loaded before griddepcontrol.wait,
+// which returns once every red of the LUT kernel is visible.
+struct FinishPair {  // operands of rows (row, row+1) that do not depend on the sums
+  float add0, add1, q0, q1;
+};
+__device__ __forceinline__ FinishPair finish_prefetch(const LaneParams& P, int64_t row) {
+  FinishPair f{0.f, 0.f, 1.f, 1.f};
+  if (row >= P.m) return f;
+  if (P.tail) {
+    const uint32_t tc = *reinterpret_cast<const uint32_t*>(P.tailp + row);  // rows row, row+1
+    for (int u = 0; u < P.tail; ++u) {
+      const float xv = __half2float(P.x[P.nb * 3 + u]);
+      f.add0 = fmaf(P.v[(tc >> (4 * u)) & 0xF], xv, f.add0);
+      f.add1 = fmaf(P.v[(tc >> (16 + 4 * u)) & 0xF], xv, f.add1);
     }
   }
-  griddep_wait();
-  griddep_launch_dependents();
-  if (!live) return;
+  if (P.scale_mode == MSG_SCALE_PER_ROW) {
+    f.q0 = load_as<float>(P.q, P.q_dtype, row);
+    if (row + 1 < P.m) f.q1 = load_as<float>(P.q, P.q_dtype, row + 1);
+  }
+  return f;
+}
+// the tail is added to the rounded fp32 sum, as the reference adds it to the
+// block sum (gemm.py:81-83); the sums are read through L2 and cleared
+__device__ __forceinline__ void finish_pair(const LaneParams& P, int64_t row, const FinishPair& f) {
+  if (row >= P.m) return;
   ulonglong2* ap = reinterpret_cast<ulonglong2*>(P.acc + row);
   const ulonglong2 raw = __ldcg(ap);
   __stcg(ap, make_ulonglong2(0ull, 0ull));
-  // the tail is added to the rounded fp32 sum, as the reference adds it to
-  // the block sum (gemm.py:81-83)
-  float y0 = __ll2float_rn((long long)raw.x) * P.fx_inv;
-  y0 = (y0 + add0) * q0;
+  const float y0 = (__ll2float_rn((long long)raw.x) * P.fx_inv + f.add0) * f.q0;
   store_as<float>(P.y, P.y_dtype, row, y0);
   if (row + 1 < P.m) {
-    float y1 = __ll2float_rn((long long)raw.y) * P.fx_inv;
-    y1 = (y1 + add1) * q1;
+    const float y1 = (__ll2float_rn((long long)raw.y) * P.fx_inv + f.add1) * f.q1;
     store_as<float>(P.y, P.y_dtype, row + 1, y1);
   }
+}
+
+__global__ void __launch_bounds__(256) lane_finish_kernel(LaneParams P) {
+  const int64_t row = ((int64_t)blockIdx.x * 256 + threadIdx.x) * 2;
+  const FinishPair f = finish_prefetch(P, row);
+  griddep_wait();
+  griddep_launch_dependents();
+  finish_pair(P, row, f);
 }
 
 // Work split: the (chunk, 32-row tile) grid linearised chunk-major,
@@ -504,8 +510,10 @@ static int launch_lane_t(const LaneParams& P, cudaStream_t s) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   MSG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, lane_lut_kernel<TPW>, P));
-  if (P.exp & 4) return MSG_OK;  // measurement: LUT kernel alone
-  // the finishing kernel, queued with PDL behind the LUT kernel
+  if (P.exp & 4) return MSG_OK;  // measurement: the LUT kernel alone
+  // the finishing kernel, queued with PDL behind the LUT kernel.  (An in-kernel
+  // grid barrier instead measured 2 us slower per call: fence + arrival +
+  // release round trips after the last CTA, vs. PDL's overlapped launch.)
   cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, ceil_div((P.m + 1) / 2, 256)));
   cfg.blockDim = dim3(256);
   cfg.dynamicSmemBytes = 0;

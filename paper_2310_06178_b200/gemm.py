@@ -119,37 +119,19 @@ def msgemm(pwm: PackedWeightMatrix, X, d: int, budget: int = DEFAULT_BUDGET,
 
     dev = _lib.require_device()
     t = _lib.torch()
-    lib = _lib.lib()
     m, k, b = pwm.m, pwm.k, int(Xm.shape[1])
     x_code = _lib.dtype_code(Xm.dtype)
     is_tensor = _lib.is_torch(X)
     on_device = is_tensor and X.is_cuda
-
-    scale_mode, group_size, q_code = _lib.SCALE_NONE, 0, _lib.F64
-    if isinstance(pwm.scales, PerRow):
-        scale_mode = _lib.SCALE_PER_ROW
-    elif isinstance(pwm.scales, PerGroup):
-        scale_mode, group_size = _lib.SCALE_PER_GROUP, pwm.scales.group_size
-    qd = pwm.device_scales(dev)
-    if qd is not None:
-        q_code = _lib.dtype_code(qd.dtype)
-        if q_code == _lib.BF16:
-            raise NotImplementedError("bfloat16 scales are not supported")
-
-    flags = int(_flags)
-    if table_dtype is not None and np.dtype(table_dtype) == np.float32:
-        flags |= _lib.FLAG_F32_ENTRIES
-    if not symmetric:
-        flags |= _lib.FLAG_NO_SYMMETRY
-
-    vals = _lib.host_doubles(pwm.codebook.values)
-    layout, sym = _lib.ctypes.c_int(0), _lib.ctypes.c_int(0)
-    ws_bytes = _lib.ctypes.c_int64(0)
-    _lib.check(lib.msg_gemm_plan(m, k, pwm.width, vals, x_code, b, d, scale_mode, group_size,
-                                 flags, _lib.ctypes.byref(layout), _lib.ctypes.byref(sym),
-                                 _lib.ctypes.byref(ws_bytes)))
-    xd = _lib.to_device(Xm, dev, non_blocking=is_tensor and not on_device and Xm.is_pinned())
-    y_dt = xd.dtype if out_dtype is None else _lib.torch_dtype_of(np.dtype(out_dtype))
+    stream = t.cuda.current_stream(dev)
+    call = _call_plan(pwm, dev, stream, b, x_code, Xm.dtype, d, table_dtype, symmetric,
+                      out_dtype, int(_flags))
+    y_dt = call.y_dtype
+    # activations on the device (host inputs go through a cached pinned + device staging pair)
+    if on_device:
+        xd = Xm if Xm.is_contiguous() else Xm.contiguous()
+    else:
+        xd = call.stage_x(Xm)
     host_out = None
     if out is not None:
         if tuple(out.shape) not in ((m, b), (m,)) or out.dtype != y_dt or not out.is_contiguous():
@@ -158,34 +140,130 @@ def msgemm(pwm: PackedWeightMatrix, X, d: int, budget: int = DEFAULT_BUDGET,
             Y = out
         else:
             host_out = out
-            Y = t.empty((m, b), dtype=y_dt, device=dev)
-    else:
+            Y = call.y_stage()
+    elif on_device:
         Y = t.empty((m, b), dtype=y_dt, device=dev)
-    y_code = _lib.dtype_code(y_dt)
+    else:
+        Y = call.y_stage()
     if m and b:
-        wrep = None
-        if layout.value != _lib.LAYOUT_NONE:
-            # a layout built by an earlier call is not written by the kernel that
-            # precedes this one: the LUT kernel may prefetch it under PDL
-            if pwm.has_device_layout(dev, d, layout.value, sym.value):
-                flags |= _lib.FLAG_STATIC_WEIGHTS
-            wrep = pwm.device_layout(dev, d, layout.value, sym.value)
-        ws = _lib.workspace(ws_bytes.value, dev,
-                            "lane" if layout.value == _lib.LAYOUT_LANE else "scratch")
-        _lib.check(lib.msg_gemm(
-            _lib.ptr(pwm.device_data(dev)), _lib.ptr(wrep), m, k, pwm.width, vals,
-            _lib.ptr(xd), x_code, b, d, scale_mode, group_size, _lib.ptr(qd), q_code,
-            _lib.ptr(Y), y_code, _lib.ptr(ws), ws.numel(), flags, _lib.stream_ptr()))
+        call.launch(xd, Y)
     if host_out is not None:          # host tensor out (e.g. pinned): one D2H, synchronous
         host_out.copy_(Y.reshape(host_out.shape))
         return host_out
-    if was_vector:
-        Y = Y.reshape(m, b)[:, 0]
     if on_device:
-        return Y
-    if is_tensor:
-        return Y.cpu()
-    return Y.cpu().numpy()
+        return Y[:, 0] if was_vector else Y
+    Yh = call.y_host(Y)               # D2H into pinned staging, then a private copy
+    Yh = Yh[:, 0] if was_vector else Yh
+    return Yh if is_tensor else Yh.numpy()
+
+
+class _CallPlan:
+    """Everything msgemm needs for one (weights, device, stream, shape, dtype,
+    options) combination, prepared once: the C-ABI plan, the repacked layout,
+    the codebook block, the workspace and the host/device staging buffers.
+    Later calls only copy activations and launch."""
+
+    def __init__(self, pwm, dev, stream, b, x_code, x_dtype, d, table_dtype, symmetric,
+                 out_dtype, flags):
+        t = _lib.torch()
+        lib = _lib.lib()
+        m, k = pwm.m, pwm.k
+        self.m, self.b, self.dev = m, b, dev
+        scale_mode, group_size, q_code = _lib.SCALE_NONE, 0, _lib.F64
+        if isinstance(pwm.scales, PerRow):
+            scale_mode = _lib.SCALE_PER_ROW
+        elif isinstance(pwm.scales, PerGroup):
+            scale_mode, group_size = _lib.SCALE_PER_GROUP, pwm.scales.group_size
+        qd = pwm.device_scales(dev)
+        if qd is not None:
+            q_code = _lib.dtype_code(qd.dtype)
+            if q_code == _lib.BF16:
+                raise NotImplementedError("bfloat16 scales are not supported")
+        if table_dtype is not None and np.dtype(table_dtype) == np.float32:
+            flags |= _lib.FLAG_F32_ENTRIES
+        if not symmetric:
+            flags |= _lib.FLAG_NO_SYMMETRY
+        self.vals = _lib.host_doubles(pwm.codebook.values)
+        layout, sym = _lib.ctypes.c_int(0), _lib.ctypes.c_int(0)
+        ws_bytes = _lib.ctypes.c_int64(0)
+        _lib.check(lib.msg_gemm_plan(m, k, pwm.width, self.vals, x_code, b, d, scale_mode,
+                                     group_size, flags, _lib.ctypes.byref(layout),
+                                     _lib.ctypes.byref(sym), _lib.ctypes.byref(ws_bytes)))
+        x_t = x_dtype if isinstance(x_dtype, t.dtype) else _lib.torch_dtype_of(x_dtype)
+        self.x_dtype = x_t
+        self.y_dtype = x_t if out_dtype is None else _lib.torch_dtype_of(np.dtype(out_dtype))
+        self.y_code = _lib.dtype_code(self.y_dtype)
+        wrep = None
+        if layout.value != _lib.LAYOUT_NONE and m and b:
+            wrep = pwm.device_layout(dev, d, layout.value, sym.value)
+            # the layout now exists before any later launch: the LUT kernel may
+            # prefetch it under PDL (it is never written by the preceding kernel)
+            flags |= _lib.FLAG_STATIC_WEIGHTS
+        ws = _lib.workspace(ws_bytes.value, dev,
+                            "lane" if layout.value == _lib.LAYOUT_LANE else "scratch")
+        # a first call that built the layout must not prefetch it: it is not static yet
+        self._first_flags = flags & ~_lib.FLAG_STATIC_WEIGHTS if wrep is not None else flags
+        self._args_head = (_lib.ptr(pwm.device_data(dev)), _lib.ptr(wrep), m, k, pwm.width,
+                           self.vals)
+        self._args_mid = (x_code, b, d, scale_mode, group_size, _lib.ptr(qd), q_code)
+        self._ws = (ws, _lib.ptr(ws), ws.numel())
+        self._flags = flags
+        self._stream = _lib.ctypes.c_void_p(stream.cuda_stream)
+        self._keep = (wrep, qd)
+        self._xs = self._xh = self._ys = self._yh = None
+        self._fn = lib.msg_gemm
+        self._launched = False
+
+    def launch(self, xd, Y):
+        flags = self._flags if self._launched else self._first_flags
+        ws, wsp, wsn = self._ws
+        _lib.check(self._fn(*self._args_head, _lib.ctypes.c_void_p(xd.data_ptr()),
+                            *self._args_mid, _lib.ctypes.c_void_p(Y.data_ptr()), self.y_code,
+                            wsp, wsn, flags, self._stream))
+        self._launched = True
+
+    def stage_x(self, Xm):
+        """Host activations -> device staging (pinned host tensors: one async H2D;
+        numpy / pageable: through a cached pinned buffer)."""
+        t = _lib.torch()
+        shape = tuple(Xm.shape)
+        if self._xs is None or tuple(self._xs.shape) != shape:
+            self._xs = t.empty(shape, dtype=self.x_dtype, device=self.dev)
+            self._xh = t.empty(shape, dtype=self.x_dtype, pin_memory=True)
+        if _lib.is_torch(Xm) and Xm.is_pinned():
+            self._xs.copy_(Xm, non_blocking=True)
+            return self._xs
+        src = t.from_numpy(np.ascontiguousarray(Xm)) if not _lib.is_torch(Xm) else Xm
+        self._xh.copy_(src)               # host memcpy into pinned memory
+        self._xs.copy_(self._xh, non_blocking=True)
+        return self._xs
+
+    def y_stage(self):
+        t = _lib.torch()
+        if self._ys is None:
+            self._ys = t.empty((self.m, self.b), dtype=self.y_dtype, device=self.dev)
+        return self._ys
+
+    def y_host(self, Y):
+        t = _lib.torch()
+        if self._yh is None:
+            self._yh = t.empty((self.m, self.b), dtype=self.y_dtype, pin_memory=True)
+        self._yh.copy_(Y)                 # D2H (synchronises the stream)
+        return self._yh.clone()           # the caller owns its result
+
+
+def _call_plan(pwm, dev, stream, b, x_code, x_dtype, d, table_dtype, symmetric, out_dtype,
+               flags) -> _CallPlan:
+    cache = pwm._device_cache
+    key = ("call", dev.index, stream.cuda_stream, b, x_code, d,
+           None if table_dtype is None else np.dtype(table_dtype).str, bool(symmetric),
+           None if out_dtype is None else np.dtype(out_dtype).str, flags)
+    plan = cache.get(key)
+    if plan is None:
+        plan = _CallPlan(pwm, dev, stream, b, x_code, x_dtype, d, table_dtype, symmetric,
+                         out_dtype, flags)
+        cache[key] = plan
+    return plan
 
 
 def msgemm_counted(pwm: PackedWeightMatrix, X, d: int, budget: int = DEFAULT_BUDGET,
