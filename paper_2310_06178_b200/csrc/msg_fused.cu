@@ -287,13 +287,13 @@ template <int D> struct FusedShape {
   static constexpr int HIB = D == 3 ? 2 : 0;   // hi plane bytes per (quad,row)
 };
 
-template <int D, typename XT, typename ET, int BC, bool SYM, int RPT>
-__global__ void __launch_bounds__(kThreads, 1) fused_lut_kernel(FusedParams P) {
+template <int D, typename XT, typename ET, int BC, bool SYM, int RPT, int NT>
+__global__ void __launch_bounds__(NT, 1) fused_lut_kernel(FusedParams P) {
   constexpr int ES = SYM ? (1 << (4 * D - 1)) : (1 << (4 * D));  // stored entries per group
   constexpr int EB = BC * (int)sizeof(ET);                        // bytes per entry
   constexpr int LOWN = D == 1 ? 1 : (D == 2 ? 16 : 256);          // combos of the low D-1 codes
   constexpr int HIN = SYM ? 8 : 16;                               // values of the top code
-  constexpr int R = kThreads * RPT;
+  constexpr int R = NT * RPT;
   constexpr int LOB = FusedShape<D>::LOB, HIB = FusedShape<D>::HIB;
   constexpr int XPT = 2;  // staged activation values per thread (<= 512 per round)
   constexpr int QUADB = 4 * ES * EB > 128 ? 4 * ES * EB : 128;  // table bytes per quad
@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_lut_kernel(FusedParams P) {
     const int nel = (int)(glast - g_first) * D * BC;
 #pragma unroll
     for (int u = 0; u < XPT; ++u) {
-      const int e = tid + u * kThreads;
+      const int e = tid + u * NT;
       float v = 0.f;
       if (e < nel) {
         const int c = e % BC, gr = e / BC;
@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_lut_kernel(FusedParams P) {
     if (tid == 0 && t + 1 < nrounds) issue(t + 1);
 #pragma unroll
     for (int u = 0; u < XPT; ++u)
-      if (tid + u * kThreads < QL * 4 * D * BC) xs[tid + u * kThreads] = xnext[u];
+      if (tid + u * NT < QL * 4 * D * BC) xs[tid + u * NT] = xnext[u];
     if (t + 1 < nrounds) load_x(t + 1, xnext);
     __syncthreads();
     if (SYM && tid < BC) {
@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_lut_kernel(FusedParams P) {
     // Work item w -> (quad, group g = w % 4, low = (w / 4) % LOWN): the lanes of
     // one store wavefront fill one whole 128-byte table row (4 groups x SPG
     // consecutive entries), so the interleaved layout is written conflict-free.
-    for (int w = tid; w < nql * 4 * LOWN; w += kThreads) {
+    for (int w = tid; w < nql * 4 * LOWN; w += NT) {
       const int qq = w / (4 * LOWN), rem = w - qq * 4 * LOWN;
       const int g = rem & 3, low = rem >> 2;
       const int gl = qq * 4 + g;
@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_lut_kernel(FusedParams P) {
       if (gcount >= 4) {
 #pragma unroll
         for (int r = 0; r < RPT; ++r) {
-          const int li = r * kThreads + tid;
+          const int li = r * NT + tid;
           if (li < rows_valid) {
             uint32_t lo, hi = 0;
             if constexpr (LOB == 4) lo = reinterpret_cast<const uint32_t*>(lo_s)[li];
@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_lut_kernel(FusedParams P) {
       } else {
 #pragma unroll
         for (int r = 0; r < RPT; ++r) {
-          const int li = r * kThreads + tid;
+          const int li = r * NT + tid;
           if (li < rows_valid) {
             uint32_t lo, hi = 0;
             if constexpr (LOB == 4) lo = reinterpret_cast<const uint32_t*>(lo_s)[li];
@@ -524,7 +524,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_lut_kernel(FusedParams P) {
   // ---- write partials [slice][i][c]
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {
-    const int li = r * kThreads + tid;
+    const int li = r * NT + tid;
     if (li < rows_valid) {
       float* dst = P.partial + ((int64_t)slice * P.m + row0 + li) * P.b + c0;
       if (c0 + BC <= P.b && BC >= 2 && (P.b % 2 == 0)) {
@@ -930,10 +930,18 @@ static FusedPlan fused_plan(int64_t m, int64_t k, int width, const double* value
   return p;
 }
 
+// Column tiles of <= 4 run the row-block kernel with 512 threads x RPT/2 rows
+// (same R = 256 * RPT rows per CTA): twice the warps to hide the gather's
+// shared-memory latency, half the accumulator registers.  At BC = 8 the
+// gather saturates the shared-memory pipe already and 256 x RPT measured
+// faster (config 5: 334 vs 341 us).
+template <int BC> constexpr int fused_nt() { return BC <= 4 ? 512 : kThreads; }
+
 template <int D, typename XT, typename ET, int BC, bool SYM, int RPT>
 static int launch_fused_t(const FusedPlan& pl, FusedParams& P, cudaStream_t s) {
+  constexpr int NT = fused_nt<BC>();
   auto kern = pl.pair ? pair_lut_kernel<D, XT, ET, BC, SYM, RPT>
-                      : fused_lut_kernel<D, XT, ET, BC, SYM, RPT>;
+                      : fused_lut_kernel<D, XT, ET, BC, SYM, RPT * kThreads / NT, NT>;
   static int configured_dev[2] = {-1, -1};  // one attribute call per kernel and device
   int dev = 0;
   cudaGetDevice(&dev);
@@ -943,7 +951,7 @@ static int launch_fused_t(const FusedPlan& pl, FusedParams& P, cudaStream_t s) {
     configured_dev[pl.pair] = dev;
   }
   dim3 grid(pl.nrow_blocks, pl.S, pl.ncol_tiles);
-  kern<<<grid, kThreads, pl.smem, s>>>(P);
+  kern<<<grid, pl.pair ? kThreads : NT, pl.smem, s>>>(P);
   MSG_LAUNCH_CHECK();
   return MSG_OK;
 }

@@ -12,10 +12,13 @@
 //     pre-swizzled fp16 X^T tile (N x 128 B) into a NS-deep smem ring;
 //   * the 128 threads dequantise their row (magic-number fp16 conversion:
 //     8 nibbles -> 4 half2 in 4 LOP3 + 4 HFMA2, K3 pre-permutes the nibbles)
-//     into the canonical K-major SWIZZLE_128B operand layout;
-//   * one thread issues 4 tcgen05.mma.kind::f16 (M128 x N x K16) with the
-//     fp32 accumulator in TMEM and commits to an mbarrier that also releases
-//     the ring slot.
+//     straight into tensor memory (tcgen05.st, 32 columns per row per k
+//     step): the A operand never touches shared memory, so at small b the
+//     kernel is bound by the int4 weight stream, not by a 4x-inflated fp16
+//     smem round trip;
+//   * one thread issues 4 tcgen05.mma.kind::f16 (M128 x N x K16) with A from
+//     TMEM, B (X^T, SW128 K-major) from smem and the fp32 accumulator in TMEM,
+//     and commits to mbarriers that release the A buffer and the ring slot.
 // The epilogue reads TMEM with tcgen05.ld (one warp per 32 rows) and writes
 // fp32 k-split partials, reduced by the shared deterministic finish kernel.
 #include <algorithm>
@@ -125,6 +128,27 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                    "r"(smem_u32(bar))
                : "memory");
 }
+// A from tensor memory ("TS" form): [d], [a], b-desc
+__device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                           uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// 32 consecutive columns of this thread's TMEM lane (warp-collective)
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
+      "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]),
+      "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]),
+      "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
@@ -140,24 +164,32 @@ struct MmaParams {
   float sub_lo, sub_hi;  // dequant constants: v = h - sub (lo lanes), v = h/16 - sub (hi lanes)
 };
 
-constexpr int kNA = 3;  // dequantised A operand buffers
+constexpr int kNA = 4;  // dequantised A operand buffers (TMEM, 32 columns each)
+
+template <int N> constexpr uint32_t dq_acc_cols() { return N < 32 ? 32 : N; }
+template <int N> constexpr uint32_t dq_tmem_cols() {
+  constexpr uint32_t need = dq_acc_cols<N>() + kNA * 32;
+  return need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : need <= 256 ? 256 : 512;
+}
 
 // Warp-specialised pipeline (256 threads):
 //   warp 0 lane 0  : TMA producer -- packed W tile + swizzled X^T tile per k step
 //                    into an NS-deep ring (full/empty mbarriers);
-//   warp 1 lane 0  : MMA issuer   -- 4 x tcgen05.mma (K=16) per k step, commits
-//                    release the A operand buffer and the ring slot;
-//   warps 4..7     : dequantisers -- one row each, int4 -> fp16 (magic numbers)
-//                    into one of kNA SW128 K-major operand buffers; afterwards
-//                    the TMEM -> register -> global epilogue (warp w reads TMEM
+//   warp 1 lane 0  : MMA issuer   -- 4 x tcgen05.mma (K=16, A from TMEM) per k
+//                    step, commits release the A buffer and the ring slot;
+//   warp 2         : TMEM allocator;
+//   warps 4..7     : dequantisers -- one row each (TMEM lane = row), int4 -> fp16
+//                    (magic numbers) into one of kNA TMEM A buffers; afterwards
+//                    the TMEM -> register -> global epilogue (warp w owns TMEM
 //                    lanes 32*(w%4)..+31).
 template <int N, int NS>
 __global__ void __launch_bounds__(256, 1) dq_mma_kernel(MmaParams P) {
   constexpr int TB = N * 128;  // B tile bytes
+  constexpr uint32_t kA0 = dq_acc_cols<N>();  // first A column (accumulator: [0, N))
+  constexpr uint32_t kCols = dq_tmem_cols<N>();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* opA = smem;                              // [kNA][16 KiB]
-  uint8_t* stB = opA + kNA * 16384;                 // [NS][TB]
+  uint8_t* stB = smem;                              // [NS][TB]
   uint8_t* stA = stB + NS * TB;                     // [NS][4 KiB]
   uint64_t* full = reinterpret_cast<uint64_t*>(stA + NS * kMmaTileA);  // [NS] TMA landed
   uint64_t* empty = full + NS;                      // [NS] slot consumed (MMA + dequant)
@@ -171,7 +203,6 @@ __global__ void __launch_bounds__(256, 1) dq_mma_kernel(MmaParams P) {
   const int64_t kt0 = split * P.kt_per_split;
   const int64_t kt1 = std::min<int64_t>(P.kt_total, kt0 + P.kt_per_split);
   const int nloc = (int)std::max<int64_t>(0, kt1 - kt0);
-  constexpr uint32_t kCols = N < 32 ? 32 : N;
 
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -217,13 +248,13 @@ __global__ void __launch_bounds__(256, 1) dq_mma_kernel(MmaParams P) {
       for (int i = 0; i < nloc; ++i) {
         const int slot = i % NS, buf = i % kNA;
         mbar_wait(&full[slot], (uint32_t)((i / NS) & 1));  // B tile landed (TMA)
-        mbar_wait(&afull[buf], (uint32_t)((i / kNA) & 1));
+        mbar_wait(&afull[buf], (uint32_t)((i / kNA) & 1));  // A written to TMEM
         tc_fence_after();
-        const uint64_t ad = umma_desc_sw128(smem_u32(opA + buf * 16384));
+        const uint32_t ta = tmem + kA0 + (uint32_t)buf * 32;
         const uint64_t bd = umma_desc_sw128(smem_u32(stB + slot * TB));
 #pragma unroll
-        for (int ks = 0; ks < kMmaBK / 16; ++ks)  // K = 16 per instruction = 32 bytes
-          mma_f16(tmem, ad + 2 * ks, bd + 2 * ks, idesc, (i > 0 || ks > 0) ? 1u : 0u);
+        for (int ks = 0; ks < kMmaBK / 16; ++ks)  // K = 16 per instruction = 8 TMEM columns
+          mma_f16_ts(tmem, ta + 8 * ks, bd + 2 * ks, idesc, (i > 0 || ks > 0) ? 1u : 0u);
         mma_commit(&aempty[buf]);
         mma_commit(&empty[slot]);
       }
@@ -231,7 +262,9 @@ __global__ void __launch_bounds__(256, 1) dq_mma_kernel(MmaParams P) {
     }
   } else if (warp >= 4) {
     // ---------------- dequantisers, then epilogue
-    const int r = tid - 128;  // tile row
+    const int quarter = warp & 3;
+    const int r = tid - 128;  // tile row = TMEM lane
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const __half2 sub_lo = __float2half2_rn(P.sub_lo);
     const __half2 sub_hi = __float2half2_rn(P.sub_hi);
     const __half2 sixteenth = __float2half2_rn(1.0f / 16.0f);
@@ -241,11 +274,10 @@ __global__ void __launch_bounds__(256, 1) dq_mma_kernel(MmaParams P) {
       const uint4* src = reinterpret_cast<const uint4*>(stA + slot * kMmaTileA + r * 32);
       const uint4 p0 = src[0], p1 = src[1];
       mbar_arrive(&empty[slot]);  // packed A copied out
-      if (i >= kNA) mbar_wait(&aempty[buf], (uint32_t)(((i / kNA) - 1) & 1));
       const uint32_t words[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
-      uint8_t* dst_row = opA + buf * 16384 + (r >> 3) * 1024 + (r & 7) * 128;
+      uint32_t o[32];  // column 4c + j holds k = 8c + 2j, 8c + 2j + 1 (lo, hi)
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {  // 16-byte chunk c = k 8c..8c+7 = word c
+      for (int c = 0; c < 8; ++c) {
         uint32_t w = words[c];
         uint32_t h[4];
         h[0] = (w & 0x000F000Fu) | 0x64006400u;
@@ -257,15 +289,19 @@ __global__ void __launch_bounds__(256, 1) dq_mma_kernel(MmaParams P) {
         __half2 v1 = __hfma2(*reinterpret_cast<__half2*>(&h[1]), sixteenth, sub_hi);
         __half2 v2 = __hsub2(*reinterpret_cast<__half2*>(&h[2]), sub_lo);
         __half2 v3 = __hfma2(*reinterpret_cast<__half2*>(&h[3]), sixteenth, sub_hi);
-        uint4 o = make_uint4(*reinterpret_cast<uint32_t*>(&v0), *reinterpret_cast<uint32_t*>(&v1),
-                             *reinterpret_cast<uint32_t*>(&v2), *reinterpret_cast<uint32_t*>(&v3));
-        *reinterpret_cast<uint4*>(dst_row + ((c ^ (r & 7)) * 16)) = o;
+        o[4 * c + 0] = *reinterpret_cast<uint32_t*>(&v0);
+        o[4 * c + 1] = *reinterpret_cast<uint32_t*>(&v1);
+        o[4 * c + 2] = *reinterpret_cast<uint32_t*>(&v2);
+        o[4 * c + 3] = *reinterpret_cast<uint32_t*>(&v3);
       }
-      fence_proxy_async();  // generic smem writes -> visible to the tensor core
+      if (i >= kNA) mbar_wait(&aempty[buf], (uint32_t)(((i / kNA) - 1) & 1));
+      tc_fence_after();
+      tmem_st32(tmem + lane_base + kA0 + (uint32_t)buf * 32, o);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
       mbar_arrive(&afull[buf]);
     }
     // ---------------- epilogue: TMEM -> registers -> fp32 partials
-    const int quarter = warp & 3;
     const int64_t row = mt * kMmaBM + quarter * 32 + lane;
     float* dst = P.partial + (split * P.m + row) * P.b;
     if (nloc > 0) {
@@ -274,7 +310,7 @@ __global__ void __launch_bounds__(256, 1) dq_mma_kernel(MmaParams P) {
 #pragma unroll
       for (int c0 = 0; c0 < N; c0 += 16) {
         uint32_t v[16];
-        const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0;
+        const uint32_t taddr = tmem + lane_base + (uint32_t)c0;
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
             "%13,%14,%15}, [%16];"
@@ -301,12 +337,22 @@ __global__ void __launch_bounds__(256, 1) dq_mma_kernel(MmaParams P) {
 
 template <int N, int NS>
 constexpr int dq_smem() {
-  return 1024 + kNA * 16384 + NS * (N * 128 + kMmaTileA) + (2 * NS + 2 * kNA + 1) * 8 + 16;
+  return 1024 + NS * (N * 128 + kMmaTileA) + (2 * NS + 2 * kNA + 1) * 8 + 16;
+}
+
+// CTAs per SM: shared memory and tensor memory (512 columns) both bound it
+template <int N, int NS>
+constexpr int dq_per_sm() {
+  const int by_smem = (227 * 1024) / dq_smem<N, NS>();
+  const int by_tmem = 512 / (int)dq_tmem_cols<N>();
+  const int v = by_smem < by_tmem ? by_smem : by_tmem;
+  return v < 1 ? 1 : (v > 4 ? 4 : v);
 }
 
 template <int N, int NS>
 static int launch_dq(const MmaParams& P, const MmaShape& S, int splits, cudaStream_t s) {
-  const int smem = dq_smem<N, NS>();
+  // request enough shared memory that no more CTAs than TMEM can serve are resident
+  const int smem = std::max(dq_smem<N, NS>(), (227 * 1024) / (dq_per_sm<N, NS>() + 1) + 1024);
   static int configured_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -321,22 +367,22 @@ static int launch_dq(const MmaParams& P, const MmaShape& S, int splits, cudaStre
   return MSG_OK;
 }
 
-constexpr int kDqStages = 4;
+constexpr int kDqStages = 6;
 
-static int dq_smem_for(int64_t npad) {
+static int dq_per_sm_for(int64_t npad) {
   switch (npad) {
-    case 16: return dq_smem<16, kDqStages>();
-    case 32: return dq_smem<32, kDqStages>();
-    case 64: return dq_smem<64, kDqStages>();
-    case 128: return dq_smem<128, kDqStages>();
+    case 16: return dq_per_sm<16, kDqStages>();
+    case 32: return dq_per_sm<32, kDqStages>();
+    case 64: return dq_per_sm<64, kDqStages>();
+    case 128: return dq_per_sm<128, kDqStages>();
   }
-  return dq_smem<256, kDqStages>();
+  return dq_per_sm<256, kDqStages>();
 }
 
 // k-splits: enough CTAs to fill every SM with as many resident CTAs as shared
 // memory allows (up to 4), each split at least 4 k tiles long
 static int mma_splits(const MmaShape& S) {
-  const int per_sm = std::max(1, std::min(4, (227 * 1024) / dq_smem_for(S.npad)));
+  const int per_sm = dq_per_sm_for(S.npad);
   int64_t sp = std::max<int64_t>(1, (int64_t)sm_count() * per_sm / std::max<int64_t>(1, S.mt));
   return (int)std::min<int64_t>(sp, std::max<int64_t>(1, S.kt / 4));
 }
