@@ -163,6 +163,7 @@ struct FusedParams {
   float s[16];  // per-code value used in tables: v[c] - beta (symmetric) or v[c]
   float beta;
   int s_exact16;        // every s[c] is exact in fp16 (fp16x2 table build allowed)
+  int early;            // MSG_FLAG_STATIC_WEIGHTS: first weight copy before griddepcontrol.wait
   int quads_per_slice;  // k-slice length in quads
   int ql;               // quads per table round
   float* partial;       // [S][m][b]
@@ -362,7 +363,13 @@ __global__ void __launch_bounds__(NT, 1) fused_lut_kernel(FusedParams P) {
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid == 0 && nrounds > 0) issue(0);
+  // Launched with PDL: the first weight copy may start before the wait only if
+  // the preceding kernel did not write the repacked weights; x is read and the
+  // partials are written only after it.  The finishing kernel may queue now.
+  if (tid == 0 && nrounds > 0 && P.early) issue(0);
+  griddep_wait();
+  griddep_launch_dependents();
+  if (tid == 0 && nrounds > 0 && !P.early) issue(0);
   float xnext[XPT];
   if (nrounds > 0) load_x(0, xnext);
 
@@ -950,9 +957,17 @@ static int launch_fused_t(const FusedPlan& pl, FusedParams& P, cudaStream_t s) {
                                         std::min(max_smem_optin(), 227 * 1024)));
     configured_dev[pl.pair] = dev;
   }
-  dim3 grid(pl.nrow_blocks, pl.S, pl.ncol_tiles);
-  kern<<<grid, pl.pair ? kThreads : NT, pl.smem, s>>>(P);
-  MSG_LAUNCH_CHECK();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(pl.nrow_blocks, pl.S, pl.ncol_tiles);
+  cfg.blockDim = dim3(pl.pair ? kThreads : NT);
+  cfg.dynamicSmemBytes = pl.smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pl.pair ? 0 : 1;  // the pair kernel has no griddepcontrol
+  MSG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, P));
   return MSG_OK;
 }
 
@@ -1099,6 +1114,7 @@ int msg_gemm(const uint8_t* packed, const uint8_t* wrep, int64_t m, int64_t k, i
     if ((double)__half2float(__float2half_rn(P.s[c])) != values[c] - beta) P.s_exact16 = 0;
   }
   P.beta = (float)beta;
+  P.early = (flags & MSG_FLAG_STATIC_WEIGHTS) ? 1 : 0;
   P.quads_per_slice = p.quads_per_slice;
   P.ql = p.ql;
   P.partial = reinterpret_cast<float*>(workspace);
