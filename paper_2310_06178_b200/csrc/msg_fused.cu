@@ -840,6 +840,66 @@ __global__ void __launch_bounds__(256) fused_finish_kernel(
   }
 }
 
+// Four consecutive outputs of one row per thread (b % 4 == 0): float4 loads
+// of every slice in slice order (deterministic), one tail code / scale per
+// row.  Same result as fused_finish_kernel<1> (fp32 adds in slice order).
+__global__ void __launch_bounds__(256) finish_vec4_kernel(
+    const float* __restrict__ partial, int S, int64_t m, int64_t b, int64_t k, int d,
+    const uint16_t* __restrict__ tailp, TailVals vals, const void* x, int x_dtype, int scale_mode,
+    const void* q, int q_dtype, void* y, int y_dtype) {
+  const int64_t total = m * b, total4 = total / 4;
+  const int64_t nb = k / d;
+  const int tail = (int)(k - nb * d);
+  griddep_launch_dependents();
+  griddep_wait();
+  for (int64_t v = (int64_t)blockIdx.x * 256 + threadIdx.x; v < total4;
+       v += (int64_t)gridDim.x * 256) {
+    const int64_t t = v * 4, i = t / b, c = t - i * b;
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4* src = reinterpret_cast<const float4*>(partial + t);
+    const int64_t stride4 = total / 4;
+    int sl = 0;
+    for (; sl + 2 < S; sl += 3) {
+      const float4 p0 = __ldcg(src + sl * stride4), p1 = __ldcg(src + (sl + 1) * stride4),
+                   p2 = __ldcg(src + (sl + 2) * stride4);
+      a.x += p0.x; a.y += p0.y; a.z += p0.z; a.w += p0.w;
+      a.x += p1.x; a.y += p1.y; a.z += p1.z; a.w += p1.w;
+      a.x += p2.x; a.y += p2.y; a.z += p2.z; a.w += p2.w;
+    }
+    for (; sl < S; ++sl) {
+      const float4 p0 = __ldcg(src + sl * stride4);
+      a.x += p0.x; a.y += p0.y; a.z += p0.z; a.w += p0.w;
+    }
+    if (tail) {
+      const uint32_t tc = tailp[i];
+      for (int u = 0; u < tail; ++u) {
+        const float w = vals.v[(tc >> (4 * u)) & 0xF];
+        const int64_t xo = (nb * d + u) * b + c;
+        a.x = fmaf(w, load_as<float>(x, x_dtype, xo), a.x);
+        a.y = fmaf(w, load_as<float>(x, x_dtype, xo + 1), a.y);
+        a.z = fmaf(w, load_as<float>(x, x_dtype, xo + 2), a.z);
+        a.w = fmaf(w, load_as<float>(x, x_dtype, xo + 3), a.w);
+      }
+    }
+    if (scale_mode == MSG_SCALE_PER_ROW) {
+      const float qs = load_as<float>(q, q_dtype, i);
+      a.x *= qs; a.y *= qs; a.z *= qs; a.w *= qs;
+    }
+    if (y_dtype == MSG_F16) {
+      __half2 h0 = __floats2half2_rn(a.x, a.y), h1 = __floats2half2_rn(a.z, a.w);
+      *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(y) + t) =
+          make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+    } else if (y_dtype == MSG_F32) {
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(y) + t) = a;
+    } else {
+      store_as<float>(y, y_dtype, t, a.x);
+      store_as<float>(y, y_dtype, t + 1, a.y);
+      store_as<float>(y, y_dtype, t + 2, a.z);
+      store_as<float>(y, y_dtype, t + 3, a.w);
+    }
+  }
+}
+
 // ============================================================================
 // host planning / dispatch
 // ============================================================================
@@ -1140,6 +1200,23 @@ int launch_finish(const float* partial, int S, int64_t m, int64_t b, int64_t k, 
                   int scale_mode, const void* q, int q_dtype, void* y, int y_dtype,
                   cudaStream_t s) {
   const int64_t total = m * b;
+  // four outputs per thread when the slice loop is short; many slices over few
+  // outputs (e.g. 137 x 8192 x 4) need the slice-group split below instead
+  if (b % 4 == 0 && scale_mode != MSG_SCALE_PER_GROUP && S >= 2 && S <= 64) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)std::max<int64_t>(
+        1, std::min<int64_t>(ceil_div(total / 4, 256), (int64_t)sm_count() * 8)));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    MSG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, finish_vec4_kernel, partial, S, m, b, k, d, tailp,
+                                      tv, x, x_dtype, scale_mode, q, q_dtype, y, y_dtype));
+    return MSG_OK;
+  }
   // slice groups per output: enough loads in flight to cover the SMs
   int sg = 1;
   while (sg < 32 && 2 * sg <= S && total * sg < (int64_t)sm_count() * 2048) sg *= 2;
