@@ -840,36 +840,55 @@ __global__ void __launch_bounds__(256) fused_finish_kernel(
   }
 }
 
-// Four consecutive outputs of one row per thread (b % 4 == 0): float4 loads
-// of every slice in slice order (deterministic), one tail code / scale per
-// row.  Same result as fused_finish_kernel<1> (fp32 adds in slice order).
+// Four consecutive outputs of one row per thread group (b % 4 == 0): float4
+// loads, slice group g (of SG) sums slices g, g+SG, ... in order, the SG
+// partial sums are combined in fixed order through shared memory --
+// deterministic run to run.  SG = 1 is the plain slice-order sum.
+template <int SG>
 __global__ void __launch_bounds__(256) finish_vec4_kernel(
     const float* __restrict__ partial, int S, int64_t m, int64_t b, int64_t k, int d,
     const uint16_t* __restrict__ tailp, TailVals vals, const void* x, int x_dtype, int scale_mode,
     const void* q, int q_dtype, void* y, int y_dtype) {
+  constexpr int OPB = 256 / SG;  // float4 outputs per block
+  __shared__ float4 red[SG > 1 ? SG : 1][OPB];
   const int64_t total = m * b, total4 = total / 4;
   const int64_t nb = k / d;
   const int tail = (int)(k - nb * d);
+  const int og = threadIdx.x % OPB, sg = threadIdx.x / OPB;
   griddep_launch_dependents();
   griddep_wait();
-  for (int64_t v = (int64_t)blockIdx.x * 256 + threadIdx.x; v < total4;
-       v += (int64_t)gridDim.x * 256) {
-    const int64_t t = v * 4, i = t / b, c = t - i * b;
+  for (int64_t v0 = (int64_t)blockIdx.x * OPB; v0 < total4; v0 += (int64_t)gridDim.x * OPB) {
+    const int64_t v = v0 + og;
     float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4* src = reinterpret_cast<const float4*>(partial + t);
-    const int64_t stride4 = total / 4;
-    int sl = 0;
-    for (; sl + 2 < S; sl += 3) {
-      const float4 p0 = __ldcg(src + sl * stride4), p1 = __ldcg(src + (sl + 1) * stride4),
-                   p2 = __ldcg(src + (sl + 2) * stride4);
-      a.x += p0.x; a.y += p0.y; a.z += p0.z; a.w += p0.w;
-      a.x += p1.x; a.y += p1.y; a.z += p1.z; a.w += p1.w;
-      a.x += p2.x; a.y += p2.y; a.z += p2.z; a.w += p2.w;
+    if (v < total4) {
+      const float4* src = reinterpret_cast<const float4*>(partial) + v;
+      int sl = sg;
+      for (; sl + 2 * SG < S; sl += 3 * SG) {
+        const float4 p0 = __ldcg(src + sl * total4), p1 = __ldcg(src + (sl + SG) * total4),
+                     p2 = __ldcg(src + (sl + 2 * SG) * total4);
+        a.x += p0.x; a.y += p0.y; a.z += p0.z; a.w += p0.w;
+        a.x += p1.x; a.y += p1.y; a.z += p1.z; a.w += p1.w;
+        a.x += p2.x; a.y += p2.y; a.z += p2.z; a.w += p2.w;
+      }
+      for (; sl < S; sl += SG) {
+        const float4 p0 = __ldcg(src + sl * total4);
+        a.x += p0.x; a.y += p0.y; a.z += p0.z; a.w += p0.w;
+      }
     }
-    for (; sl < S; ++sl) {
-      const float4 p0 = __ldcg(src + sl * stride4);
-      a.x += p0.x; a.y += p0.y; a.z += p0.z; a.w += p0.w;
+    if constexpr (SG > 1) {
+      red[sg][og] = a;
+      __syncthreads();
+      if (sg == 0) {
+#pragma unroll
+        for (int g = 1; g < SG; ++g) {
+          const float4 r = red[g][og];
+          a.x += r.x; a.y += r.y; a.z += r.z; a.w += r.w;
+        }
+      }
+      __syncthreads();
     }
+    if (sg != 0 || v >= total4) continue;
+    const int64_t t = v * 4, i = t / b, c = t - i * b;
     if (tail) {
       const uint32_t tc = tailp[i];
       for (int u = 0; u < tail; ++u) {
@@ -1200,12 +1219,15 @@ int launch_finish(const float* partial, int S, int64_t m, int64_t b, int64_t k, 
                   int scale_mode, const void* q, int q_dtype, void* y, int y_dtype,
                   cudaStream_t s) {
   const int64_t total = m * b;
-  // four outputs per thread when the slice loop is short; many slices over few
-  // outputs (e.g. 137 x 8192 x 4) need the slice-group split below instead
-  if (b % 4 == 0 && scale_mode != MSG_SCALE_PER_GROUP && S >= 2 && S <= 64) {
+  // four outputs per thread group; slices split over SG groups when there are
+  // few outputs per SM (e.g. 137 slices x 8192 x 4)
+  if (b % 4 == 0 && scale_mode != MSG_SCALE_PER_GROUP && S >= 2) {
+    int sg = 1;
+    while (sg < 16 && 2 * sg <= S && (total / 4) * sg < (int64_t)sm_count() * 512) sg *= 2;
+    const int opb = 256 / sg;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)std::max<int64_t>(
-        1, std::min<int64_t>(ceil_div(total / 4, 256), (int64_t)sm_count() * 8)));
+        1, std::min<int64_t>(ceil_div(total / 4, opb), (int64_t)sm_count() * 8)));
     cfg.blockDim = dim3(256);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -1213,8 +1235,17 @@ int launch_finish(const float* partial, int S, int64_t m, int64_t b, int64_t k, 
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    MSG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, finish_vec4_kernel, partial, S, m, b, k, d, tailp,
-                                      tv, x, x_dtype, scale_mode, q, q_dtype, y, y_dtype));
+#define MSG_FIN4(G)                                                                            \
+  MSG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, finish_vec4_kernel<G>, partial, S, m, b, k, d, tailp, \
+                                    tv, x, x_dtype, scale_mode, q, q_dtype, y, y_dtype))
+    switch (sg) {
+      case 1: MSG_FIN4(1); break;
+      case 2: MSG_FIN4(2); break;
+      case 4: MSG_FIN4(4); break;
+      case 8: MSG_FIN4(8); break;
+      default: MSG_FIN4(16); break;
+    }
+#undef MSG_FIN4
     return MSG_OK;
   }
   // slice groups per output: enough loads in flight to cover the SMs
