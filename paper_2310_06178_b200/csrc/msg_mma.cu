@@ -164,7 +164,7 @@ struct MmaParams {
   float sub_lo, sub_hi;  // dequant constants: v = h - sub (lo lanes), v = h/16 - sub (hi lanes)
 };
 
-constexpr int kNA = 4;  // dequantised A operand buffers (TMEM, 32 columns each)
+constexpr int kNA = 3;  // dequantised A operand buffers (TMEM, 32 columns each; 3 keeps N<=32 at 128 columns = 4 CTAs/SM)
 
 template <int N> constexpr uint32_t dq_acc_cols() { return N < 32 ? 32 : N; }
 template <int N> constexpr uint32_t dq_tmem_cols() {
