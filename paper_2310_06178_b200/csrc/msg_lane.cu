@@ -121,6 +121,8 @@ __device__ __forceinline__ uint32_t funnel_r(uint32_t lo, uint32_t hi) {
   return r;
 }
 
+constexpr int kMaxLaneCtas = 256;  // >= SM count
+
 struct LaneParams {
   const uint8_t* body;
   const uint16_t* tailp;  // (m,) tail codes when k % 3 != 0, else nullptr
@@ -140,6 +142,7 @@ struct LaneParams {
   uint32_t ones;    // 0x3C003C00: two fp16 +1.0
   int early;        // MSG_FLAG_STATIC_WEIGHTS: stream weights before griddepcontrol.wait
   int exp;          // 4: LUT kernel only (measurement); other bits: experiments
+  int bounds[kMaxLaneCtas + 1];  // CTA c owns global tiles [bounds[c], bounds[c+1])
 };
 
 constexpr int kLaneThreads = 512;
@@ -215,7 +218,7 @@ constexpr int kTableBytes = 128 * 1024;
 constexpr int kTileBytes = 1536;             // one 32-row tile of one chunk
 constexpr int kRing = 4;                     // tiles in flight per warp (TMA ring of batches)
 constexpr int kNW = kLaneThreads / 32;
-constexpr int kLaneSmem = kTableBytes + kNW * kRing * kTileBytes + kNW * kRing * 8 + 16;
+constexpr int kLaneSmem = kTableBytes + kNW * kRing * kTileBytes + kNW * kRing * 8 + 16 + 448;
 
 // Y from the fixed-point row sums: k % 3 tail, per-row scale, Y's dtype
 // (gemm.py:70-86), two rows (16 B of sums) per thread, in a kernel queued
@@ -267,7 +270,9 @@ __global__ void __launch_bounds__(256) lane_finish_kernel(LaneParams P) {
 
 // Work split: the (chunk, 32-row tile) grid linearised chunk-major,
 // g = chunk * ntiles + tile -- which is also the order of the tiles in HBM --
-// is cut into one contiguous range per CTA (one CTA per SM).  A range covers
+// is cut into one contiguous range per CTA (one CTA per SM), balanced on the
+// host so that a range that pays for two table builds gets fewer tiles
+// (lane_bounds).  A range covers
 // one or two chunks ("segments"); per segment the CTA builds the chunk's
 // tables once and warp w takes a contiguous run of the segment, TPW tiles per batch.  Each warp streams its
 // batches through a ring of kRing/TPW shared-memory slots, one cp.async.bulk
@@ -289,13 +294,17 @@ __global__ void __launch_bounds__(kLaneThreads, 1) lane_lut_kernel(LaneParams P)
                    warp * kRing;
   float* corr_s = reinterpret_cast<float*>(smem + kTableBytes + kNW * kRing * kTileBytes +
                                            kNW * kRing * 8);
+  __half* xbuf = reinterpret_cast<__half*>(corr_s + 4);  // [2][96] staged activations
   if (tid == 0 && smem_u32(smem) != kSmemBase) __trap();  // the LDS immediate assumes it
   const int nt = P.ntiles;
-  const int64_t G = (int64_t)P.nchunk * nt;  // < 2^31 (checked at launch)
-  const int G0 = (int)(G * blockIdx.x / gridDim.x), G1 = (int)(G * (blockIdx.x + 1) / gridDim.x);
+  const int G0 = P.bounds[blockIdx.x], G1 = P.bounds[blockIdx.x + 1];  // G < 2^31
   const unsigned long long t_start = P.trace ? global_ns() : 0ull;
   unsigned long long t_build = 0, t_wait = 0, t_loop = 0, t_count = 0;  // trace phases
 
+  if (tid == 0 && P.trace) {
+    *reinterpret_cast<unsigned long long*>(corr_s + 100) = ~0ull;
+    *reinterpret_cast<unsigned long long*>(corr_s + 102) = 0ull;
+  }
   if (lane == 0)
     for (int i = 0; i < kSlots; ++i) mbar_init(&bars[i], 1);
   fence_mbar_init();
@@ -338,18 +347,22 @@ __global__ void __launch_bounds__(kLaneThreads, 1) lane_lut_kernel(LaneParams P)
     }
   };
 
-  // activations are prefetched as raw fp16 and converted at the build
-  auto load_x = [&](int c, __half& x0, __half& x1, __half& x2) {
-    x0 = x1 = x2 = __float2half(0.f);
-    const int64_t g = c * 32 + lane;
-    if (c < P.nchunk && g < P.nb) {
-      const __half* xp = P.x + 3 * g;
-      x0 = xp[0];
-      x1 = xp[1];
-      x2 = xp[2];
+  // Activations of a chunk (96 fp16 = 48 words, zero beyond 3 nb) are copied
+  // global -> shared with cp.async by warps 0-1 one chunk ahead, so no build
+  // waits on a global load (register prefetches were being sunk by the
+  // compiler next to their use).  xbuf[c & 1] holds chunk c.
+  auto stage_x = [&](int c) {
+    if (tid < 48 && c < P.nchunk) {
+      const int64_t e = (int64_t)c * 96 + 2 * tid;   // first element of this word
+      const int64_t lim = P.nb * 3;                   // elements that belong to groups
+      const int bytes = e + 2 <= lim ? 4 : (e + 1 <= lim ? 2 : 0);
+      const __half* src = P.x + (bytes ? e : 0);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(xbuf + (c & 1) * 96 + 2 * tid)),
+                   "l"(src), "r"(bytes)
+                   : "memory");
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  __half xn0, xn1, xn2;
   // Launched with PDL: the prologue overlaps the previous kernel's tail.  The
   // weight stream may start before the wait only if the previous kernel did
   // not write it; x and acc are touched only after the wait.
@@ -357,19 +370,32 @@ __global__ void __launch_bounds__(kLaneThreads, 1) lane_lut_kernel(LaneParams P)
   griddep_wait();
   griddep_launch_dependents();
   if (!P.early) refill();
-  load_x(G0 / nt, xn0, xn1, xn2);
+  stage_x(G0 / nt);
+  stage_x(G0 / nt + 1);
 
   const uint32_t lane4 = (uint32_t)lane << 2;
   const uint32_t ones = P.ones;  // 0x3C003C00 from the parameter block (one LOP3 for S)
   for (int seg_b = G0; seg_b < G1;) {
     const int c = seg_b / nt;
     const int seg_e = min(G1, (c + 1) * nt);
-    const float x0 = __half2float(xn0), x1 = __half2float(xn1), x2 = __half2float(xn2);
-    load_x(c + 1, xn0, xn1, xn2);  // prefetch the next chunk's activations
     // ---- build chunk c's 32 bank-private half tables (groups beyond nb get
     // x = 0, i.e. all-zero tables, so padded positions contribute nothing)
+    if (P.trace && seg_b != G0) {  // earliest / latest warp arrival at the 2nd build
+      const unsigned long long ta = global_ns();
+      if (lane == 0) {
+        atomicMin(reinterpret_cast<unsigned long long*>(corr_s + 100), ta);
+        atomicMax(reinterpret_cast<unsigned long long*>(corr_s + 102), ta);
+      }
+    }
+    asm volatile("cp.async.wait_group 1;" ::: "memory");  // chunk c landed (c+1 may be in flight)
     __syncthreads();
+    const __half* xc = xbuf + (c & 1) * 96 + 3 * lane;
+    const float x0 = __half2float(xc[0]), x1 = __half2float(xc[1]), x2 = __half2float(xc[2]);
     const unsigned long long tb0 = P.trace ? global_ns() : 0ull;
+    if (P.trace && seg_b != G0) {
+      t_wait = *reinterpret_cast<unsigned long long*>(corr_s + 100);
+      t_count = *reinterpret_cast<unsigned long long*>(corr_s + 102);
+    }
     {
       if (warp == 0) {
         float sx = x0 + x1 + x2;
@@ -401,6 +427,7 @@ __global__ void __launch_bounds__(kLaneThreads, 1) lane_lut_kernel(LaneParams P)
     __syncthreads();
     if (P.trace) t_build += global_ns() - tb0;
     const float corr = *corr_s;
+    stage_x(c + 2);  // xbuf[c & 1] is free again: chunk c + 2 goes there
     int cb, ce;
     run_of(seg_b, seg_e, cb, ce);
     for (int b0 = cb; b0 < ce; b0 += TPW) {
@@ -487,8 +514,48 @@ int64_t lane_workspace_bytes(int64_t m, int64_t k) {
   return align256l(L.ntiles * 32 * 8);
 }
 
+// Split the chunk-major tile sequence into `grid` contiguous CTA ranges that
+// balance the estimated time: every tile costs 1, every table build (one per
+// chunk a range touches) costs kBuildTiles -- the smallest target T whose
+// greedy packing needs <= grid ranges, found by bisection.
+static int lane_bounds(int64_t nchunk, int64_t nt, int grid, int* bounds) {
+  // measured (tools/trace_cta.py): a second segment costs its 128 KiB table
+  // build (~10 tiles of lookups) plus the barrier that waits for the slowest
+  // warp of the first segment (up to one 2-tile batch per warp) and the
+  // refilled weight ring -- ~40 tiles in all at config 4
+  constexpr int64_t kBuildTiles = 40;
+  const int64_t G = nchunk * nt;
+  auto pack = [&](int64_t T, int* out) {  // ranges needed at target T (fills out when given)
+    int n = 0;
+    int64_t g = 0;
+    while (g < G) {
+      if (out) out[n] = (int)g;
+      ++n;
+      int64_t cost = 0;
+      while (g < G) {
+        const int64_t chunk_end = (g / nt + 1) * nt;
+        const int64_t room = T - cost - kBuildTiles;  // tiles affordable after this build
+        if (room <= 0 && cost > 0) break;
+        const int64_t take = std::min<int64_t>(chunk_end - g, std::max<int64_t>(room, 1));
+        cost += kBuildTiles + take;
+        g += take;
+        if (g < chunk_end) break;  // range full inside this chunk
+      }
+    }
+    if (out) out[n] = (int)G;
+    return n;
+  };
+  int64_t lo = (G + grid - 1) / grid, hi = G + kBuildTiles * nchunk + 1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) / 2;
+    if (pack(mid, nullptr) <= grid) hi = mid; else lo = mid + 1;
+  }
+  const int n = pack(lo, bounds);
+  return n;  // CTAs actually used (<= grid)
+}
+
 template <int TPW>
-static int launch_lane_t(const LaneParams& P, cudaStream_t s) {
+static int launch_lane_t(LaneParams& P, cudaStream_t s) {
   static int configured_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -498,7 +565,8 @@ static int launch_lane_t(const LaneParams& P, cudaStream_t s) {
     configured_dev = dev;
   }
   const int64_t G = (int64_t)P.nchunk * P.ntiles;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(G, sm_count()));
+  const int want = (int)std::max<int64_t>(1, std::min<int64_t>({G, sm_count(), kMaxLaneCtas}));
+  const int grid = lane_bounds(P.nchunk, P.ntiles, want, P.bounds);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kLaneThreads);

@@ -34,7 +34,8 @@ t0 = tr[:, 1].min()
 start = (tr[:, 1] - t0) / 1e3
 end = (tr[:, 2] - t0) / 1e3
 dur = end - start
-build, wait = tr[:, 4] / 1e3, tr[:, 5] / 1e3
+build = tr[:, 4] / 1e3
+wait = np.where(tr[:, 5] > 0, (tr[:, 5] - t0) / 1e3, np.nan)  # lane: thread 0 at the 2nd build
 loop = np.where(tr[:, 6] > 0, (tr[:, 6] - t0) / 1e3, np.nan)
 count = np.where(tr[:, 7] > 0, (tr[:, 7] - t0) / 1e3, np.nan)
 print(f"{name}: {len(tr)} CTAs; start us min/max {start.min():.2f}/{start.max():.2f}; "
