@@ -518,12 +518,7 @@ int64_t lane_workspace_bytes(int64_t m, int64_t k) {
 // balance the estimated time: every tile costs 1, every table build (one per
 // chunk a range touches) costs kBuildTiles -- the smallest target T whose
 // greedy packing needs <= grid ranges, found by bisection.
-static int lane_bounds(int64_t nchunk, int64_t nt, int grid, int* bounds) {
-  // measured (tools/trace_cta.py): a second segment costs its 128 KiB table
-  // build (~10 tiles of lookups) plus the barrier that waits for the slowest
-  // warp of the first segment (up to one 2-tile batch per warp) and the
-  // refilled weight ring -- ~40 tiles in all at config 4
-  constexpr int64_t kBuildTiles = 40;
+static int lane_bounds(int64_t nchunk, int64_t nt, int grid, int* bounds, int64_t kBuildTiles) {
   const int64_t G = nchunk * nt;
   auto pack = [&](int64_t T, int* out) {  // ranges needed at target T (fills out when given)
     int n = 0;
@@ -566,7 +561,10 @@ static int launch_lane_t(LaneParams& P, cudaStream_t s) {
   }
   const int64_t G = (int64_t)P.nchunk * P.ntiles;
   const int want = (int)std::max<int64_t>(1, std::min<int64_t>({G, sm_count(), kMaxLaneCtas}));
-  const int grid = lane_bounds(P.nchunk, P.ntiles, want, P.bounds);
+  // a second segment costs its table build (~10 tiles of lookups) plus the
+  // barrier that waits for the slowest warp's last batch and the refilled
+  // ring: ~40 tiles measured at config 4 (tools/trace_cta.py)
+  const int grid = lane_bounds(P.nchunk, P.ntiles, want, P.bounds, 40);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kLaneThreads);
@@ -624,9 +622,10 @@ int launch_lane(const uint8_t* wrep, int64_t m, int64_t k, const double* values,
   P.ones = 0x3C003C00u;
   P.early = early ? 1 : 0;
   P.exp = exp;
-  // 2 tiles per warp batch (ILP) when every CTA gets at least two batches per
-  // warp, else 1 (finer split, better balance on small problems)
-  if (L.nchunk * L.ntiles >= 4LL * kNW * sm_count()) return launch_lane_t<2>(P, s);
+  // One tile per warp batch: measured faster than 2-tile batches (whose ILP
+  // is not needed with 16 warps) at configs 2 and 4 -- warps finish a segment
+  // within one tile of each other.  Experiment bit 16 selects 2-tile batches.
+  if (exp & 16) return launch_lane_t<2>(P, s);
   return launch_lane_t<1>(P, s);
 }
 
