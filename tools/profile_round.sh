@@ -21,4 +21,8 @@ ncu --set full --clock-control none --import-source on -k regex:lane_lut -s 2 -c
 $B --config cfg4b1 > /dev/null 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:dq_mma -s 2 -c 1 \
     -o $O/full_cfg4b1_dq_mma $B --config cfg4b1 > /dev/null 2>&1
+# the comparison kernel where it is tensor-bound (b = 256)
+$B --config cfg4b256 > /dev/null 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:dq_mma -s 2 -c 1 \
+    -o $O/full_cfg4b256_dq_mma $B --config cfg4b256 > /dev/null 2>&1
 ls -la $O
