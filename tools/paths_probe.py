@@ -1,7 +1,7 @@
 """Small msgemm calls through every kernel family (odd shapes, tails), each
 checked against the oracle -- a quick all-paths probe.
 
-    python tools/sanitize_probe.py
+    python tools/paths_probe.py
 """
 import sys
 
