@@ -272,14 +272,14 @@ __global__ void __launch_bounds__(256) lane_finish_kernel(LaneParams P) {
 // g = chunk * ntiles + tile -- which is also the order of the tiles in HBM --
 // is cut into one contiguous range per CTA (one CTA per SM), balanced on the
 // host so that a range that pays for two table builds gets fewer tiles
-// (lane_bounds).  A range covers
-// one or two chunks ("segments"); per segment the CTA builds the chunk's
-// tables once and warp w takes a contiguous run of the segment, TPW tiles per batch.  Each warp streams its
-// batches through a ring of kRing/TPW shared-memory slots, one cp.async.bulk
-// and one mbarrier per batch (lane 0 issues), so the weight stream keeps
-// kNW*kRing*1.5 KB in flight per SM through the table builds.
+// (lane_bounds).  A range covers one or two chunks ("segments"); per segment
+// the CTA builds the chunk's tables once and warp w takes a contiguous run of
+// the segment, TPW tiles per batch.  Each warp streams its batches through a
+// ring of kRing/TPW shared-memory slots, one cp.async.bulk and one mbarrier
+// per batch (lane 0 issues), so the weight stream keeps kNW*kRing*1.5 KB in
+// flight per SM through the table builds.
 //
-// Cross-CTA reduction (no partial buffer, no second kernel): every lane rounds
+// Cross-CTA reduction (a partial buffer-free int64 sum): every lane rounds
 // its row's chunk sum onto the fixed-point grid 2^-F and adds it with one
 // 64-bit integer red into acc[row]; integer addition is associative, so Y is
 // bitwise deterministic whatever the arrival order.  lane_finish_kernel,
