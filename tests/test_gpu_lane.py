@@ -144,3 +144,42 @@ def test_side_stream():
         y = mg.msgemm(pwm, torch.from_numpy(x).cuda(), 3)
     s.synchronize()
     assert np.array_equal(y.cpu().numpy().view(np.uint16), ref.view(np.uint16))
+
+
+@pytest.mark.parametrize("cbname", ["uint4", "custom_antisym"])
+def test_lane_other_antisymmetric_codebooks(cbname):
+    """uint4 (beta = 7.5) and a custom antisymmetric codebook take the lane path
+    with their own symmetry shift and fixed-point grid."""
+    if cbname == "uint4":
+        cb = mg.uint4_codebook()
+        vals = np.arange(16, dtype=np.float64)
+    else:
+        vals = np.array([-7.5, -6.0, -4.25, -3.0, -2.0, -1.5, -0.75, -0.25,
+                         0.25, 0.75, 1.5, 2.0, 3.0, 4.25, 6.0, 7.5])
+        # antisymmetric: v[c] + v[~c] == 0
+        assert np.allclose(vals + vals[::-1], 0)
+        cb = mg.custom_codebook(list(vals))
+    rng = np.random.default_rng(21)
+    m, k = 640, 3001
+    codes = rng.integers(0, 16, (m, k), dtype=np.uint8)
+    pwm = mg.from_codes(codes, cb)
+    x = rng.standard_normal(k).astype(np.float16)
+    vals_c = _lib.host_doubles(cb.values)
+    lay, sym, ws = ctypes.c_int(), ctypes.c_int(), ctypes.c_int64()
+    _lib.check(_lib.lib().msg_gemm_plan(m, k, 4, vals_c, _lib.F16, 1, 3, 0, 0, 0,
+                                        ctypes.byref(lay), ctypes.byref(sym), ctypes.byref(ws)))
+    assert lay.value == _lib.LAYOUT_LANE
+    y = mg.msgemm(pwm, x, 3)
+    W = vals[codes.astype(np.int64)]
+    assert orc.rel_error(y, W, x) <= 2e-3
+
+
+def test_lane_long_k():
+    """Many chunks (k = 60000: 625 chunks) keep the fixed-point grid inside int64."""
+    rng = np.random.default_rng(22)
+    m, k = 96, 60000
+    pwm = mg.from_codes(rng.integers(0, 16, (m, k), dtype=np.uint8), mg.int4_codebook())
+    x = rng.standard_normal(k).astype(np.float16)
+    y = mg.msgemm(pwm, x, 3)
+    W = orc.dense(pwm.data, k, 4, orc.int4_values())
+    assert orc.rel_error(y, W, x) <= 2e-3
