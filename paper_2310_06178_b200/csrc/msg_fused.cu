@@ -315,8 +315,10 @@ __global__ void __launch_bounds__(NT, 1) fused_lut_kernel(FusedParams P) {
   uint8_t* tab = smem;                                                   // [QL*4][ES][BC] ET
   uint8_t* stage = tab + (size_t)QL * QUADB;                             // [2][QL][R] lo,hi
   const size_t stage_bytes = (size_t)QL * R * (LOB + HIB);
-  float* xs = reinterpret_cast<float*>(stage + 2 * stage_bytes);         // [QL*4*D][BC]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(xs + QL * 4 * D * BC);   // [2]
+  constexpr int XN_MAX = 2 * NT;  // staged activations per round (QL*4*D*BC <= 2 NT)
+  const int XN = QL * 4 * D * BC;
+  float* xs0 = reinterpret_cast<float*>(stage + 2 * stage_bytes);       // [2][XN]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(xs0 + 2 * XN);           // [2]
 
   const uint8_t* lo_plane = P.wrep + P.lo_off;
   const uint8_t* hi_plane = P.wrep + P.hi_off;
@@ -370,8 +372,18 @@ __global__ void __launch_bounds__(NT, 1) fused_lut_kernel(FusedParams P) {
   griddep_wait();
   griddep_launch_dependents();
   if (tid == 0 && nrounds > 0 && !P.early) issue(0);
+  // activations, double-buffered one round ahead: round t reads xs0[t & 1],
+  // written during round t - 1 (or here), so no barrier sits between the
+  // staging and the build
   float xnext[XPT];
-  if (nrounds > 0) load_x(0, xnext);
+  if (nrounds > 0) {
+    load_x(0, xnext);
+#pragma unroll
+    for (int u = 0; u < XPT; ++u)
+      if (tid + u * NT < XN) xs0[tid + u * NT] = xnext[u];
+  }
+  if (nrounds > 1) load_x(1, xnext);
+  static_assert(XPT * NT >= XN_MAX, "staging capacity");
 
   float acc[RPT][BC];
 #pragma unroll
@@ -393,13 +405,15 @@ __global__ void __launch_bounds__(NT, 1) fused_lut_kernel(FusedParams P) {
     const int64_t g_first = qa * 4;
     const int ngroups = (int)((int64_t)nql * 4 < P.nb - g_first ? (int64_t)nql * 4 : P.nb - g_first);
 
-    __syncthreads();  // round t-1 finished with tab, xs and stage[(t+1)&1]
+    __syncthreads();  // round t-1 finished with tab, xs0[(t+1)&1] and stage[(t+1)&1]
     if (tid == 0 && t + 1 < nrounds) issue(t + 1);
+    float* xs = xs0 + (t & 1) * XN;
+    if (t + 1 < nrounds) {
 #pragma unroll
-    for (int u = 0; u < XPT; ++u)
-      if (tid + u * NT < QL * 4 * D * BC) xs[tid + u * NT] = xnext[u];
-    if (t + 1 < nrounds) load_x(t + 1, xnext);
-    __syncthreads();
+      for (int u = 0; u < XPT; ++u)
+        if (tid + u * NT < XN) xs0[((t + 1) & 1) * XN + tid + u * NT] = xnext[u];
+    }
+    if (t + 2 < nrounds) load_x(t + 2, xnext);
     if (SYM && tid < BC) {
       float sacc = 0.f;
       for (int gr = 0; gr < ngroups * D; ++gr) sacc += xs[gr * BC + tid];
@@ -518,11 +532,11 @@ __global__ void __launch_bounds__(NT, 1) fused_lut_kernel(FusedParams P) {
   // ---- fold this slice's symmetry correction beta * sum(x) into every row
   if constexpr (SYM) {
     __syncthreads();
-    if (tid < BC) xs[tid] = P.beta * corr;
+    if (tid < BC) xs0[tid] = P.beta * corr;
     __syncthreads();
     float cv[BC];
 #pragma unroll
-    for (int c = 0; c < BC; ++c) cv[c] = xs[c];
+    for (int c = 0; c < BC; ++c) cv[c] = xs0[c];
 #pragma unroll
     for (int r = 0; r < RPT; ++r)
 #pragma unroll
@@ -1002,7 +1016,7 @@ static FusedPlan fused_plan(int64_t m, int64_t k, int width, const double* value
   // staged activations: at most 2 per thread per round
   while (ql > 1 && ql * 4 * d * bc > 2 * kThreads) --ql;
   p.ql = (int)ql;
-  p.smem = p.ql * quad_bytes(bc) + 16;
+  p.smem = p.ql * quad_bytes(bc) + p.ql * 4 * d * bc * 4 + 16;  // + second activation buffer
   // double-buffered pair kernel when two 2-group table buffers fit
   const int64_t pairb = std::max<int64_t>(2 * ES * bc * esize, 128);
   const int64_t pair_smem = 2 * pairb + 2 * (int64_t)kThreads * p.rpt * (lob + hib) +
