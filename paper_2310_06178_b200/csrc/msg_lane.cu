@@ -30,6 +30,8 @@
 // more than the minimum.
 #include <algorithm>
 #include <cmath>
+#include <utility>
+#include <vector>
 
 #include "msg_common.cuh"
 
@@ -564,7 +566,24 @@ static int launch_lane_t(LaneParams& P, cudaStream_t s) {
   // a second segment costs its table build (~10 tiles of lookups) plus the
   // barrier that waits for the slowest warp's last batch and the refilled
   // ring: ~40 tiles measured at config 4 (tools/trace_cta.py)
-  const int grid = lane_bounds(P.nchunk, P.ntiles, want, P.bounds, 40);
+  // the split depends only on the shape: computed once per (nchunk, ntiles,
+  // grid) and reused (the bisection costs ~10 us of host time per call)
+  struct BoundsKey { int64_t nchunk, nt; int grid; };
+  struct BoundsVal { int n; std::vector<int> b; };
+  static thread_local std::vector<std::pair<BoundsKey, BoundsVal>> cache;
+  const BoundsVal* hit = nullptr;
+  for (const auto& e : cache)
+    if (e.first.nchunk == P.nchunk && e.first.nt == P.ntiles && e.first.grid == want) hit = &e.second;
+  if (!hit) {
+    BoundsVal v;
+    v.b.resize(want + 1);
+    v.n = lane_bounds(P.nchunk, P.ntiles, want, v.b.data(), 40);
+    if (cache.size() >= 64) cache.erase(cache.begin());
+    cache.push_back({BoundsKey{P.nchunk, P.ntiles, want}, std::move(v)});
+    hit = &cache.back().second;
+  }
+  const int grid = hit->n;
+  std::copy(hit->b.begin(), hit->b.begin() + grid + 1, P.bounds);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kLaneThreads);

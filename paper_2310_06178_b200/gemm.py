@@ -15,6 +15,7 @@ CUDA tensors with no host round trip.  There is no CPU fallback.
 
 from __future__ import annotations
 
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -127,32 +128,27 @@ def msgemm(pwm: PackedWeightMatrix, X, d: int, budget: int = DEFAULT_BUDGET,
     call = _call_plan(pwm, dev, stream, b, x_code, Xm.dtype, d, table_dtype, symmetric,
                       out_dtype, int(_flags))
     y_dt = call.y_dtype
-    # activations on the device (host inputs go through a cached pinned + device staging pair)
-    if on_device:
+    if out is not None and (tuple(out.shape) not in ((m, b), (m,)) or out.dtype != y_dt
+                            or not out.is_contiguous()):
+        raise ValueError("out must be a contiguous tensor of shape (m, b) and Y's dtype")
+    host_out = out if (out is not None and not out.is_cuda) else None
+    if on_device and host_out is None:  # device in, device out: no staging involved
         xd = Xm if Xm.is_contiguous() else Xm.contiguous()
-    else:
-        xd = call.stage_x(Xm)
-    host_out = None
-    if out is not None:
-        if tuple(out.shape) not in ((m, b), (m,)) or out.dtype != y_dt or not out.is_contiguous():
-            raise ValueError("out must be a contiguous tensor of shape (m, b) and Y's dtype")
-        if out.is_cuda:
-            Y = out
-        else:
-            host_out = out
-            Y = call.y_stage()
-    elif on_device:
-        Y = t.empty((m, b), dtype=y_dt, device=dev)
-    else:
+        Y = out if out is not None else t.empty((m, b), dtype=y_dt, device=dev)
+        if m and b:
+            call.launch(xd, Y)
+        return Y[:, 0] if (was_vector and out is None) else Y
+    # host activations and/or host output: the plan's pinned + device staging
+    # buffers are shared by calls on this stream, so one call uses them at a time
+    with call.lock:
+        xd = (Xm if Xm.is_contiguous() else Xm.contiguous()) if on_device else call.stage_x(Xm)
         Y = call.y_stage()
-    if m and b:
-        call.launch(xd, Y)
-    if host_out is not None:          # host tensor out (e.g. pinned): one D2H, synchronous
-        host_out.copy_(Y.reshape(host_out.shape))
-        return host_out
-    if on_device:
-        return Y[:, 0] if was_vector else Y
-    Yh = call.y_host(Y)               # D2H into pinned staging, then a private copy
+        if m and b:
+            call.launch(xd, Y)
+        if host_out is not None:      # host tensor out (e.g. pinned): one D2H, synchronous
+            host_out.copy_(Y.reshape(host_out.shape))
+            return host_out
+        Yh = call.y_host(Y)           # D2H into pinned staging, then a private copy
     Yh = Yh[:, 0] if was_vector else Yh
     return Yh if is_tensor else Yh.numpy()
 
@@ -213,6 +209,7 @@ class _CallPlan:
         self._xs = self._xh = self._ys = self._yh = None
         self._fn = lib.msg_gemm
         self._launched = False
+        self.lock = threading.Lock()
 
     def launch(self, xd, Y):
         flags = self._flags if self._launched else self._first_flags

@@ -183,3 +183,35 @@ def test_lane_long_k():
     y = mg.msgemm(pwm, x, 3)
     W = orc.dense(pwm.data, k, 4, orc.int4_values())
     assert orc.rel_error(y, W, x) <= 2e-3
+
+
+def test_concurrent_host_calls_share_staging_safely():
+    """Host-staged calls from several Python threads on one plan serialise on
+    its staging buffers (results match the single-threaded ones)."""
+    import threading
+    pwm, x, rng = _case(1024, 2048, 23)
+    xs = [rng.standard_normal(2048).astype(np.float16) for _ in range(8)]
+    refs = [mg.msgemm(pwm, v, 3) for v in xs]
+    outs = [None] * len(xs)
+
+    def work(i):
+        for _ in range(5):
+            outs[i] = mg.msgemm(pwm, xs[i], 3)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(len(xs))]
+    for t_ in th:
+        t_.start()
+    for t_ in th:
+        t_.join()
+    for o, r in zip(outs, refs):
+        assert np.array_equal(o.view(np.uint16), r.view(np.uint16))
+
+
+def test_device_out_vector():
+    import torch
+    pwm, x, _ = _case(300, 600, 24)
+    ref = mg.msgemm(pwm, x, 3)
+    out = torch.empty(300, dtype=torch.float16, device="cuda")
+    y = mg.msgemm(pwm, torch.from_numpy(x).cuda(), 3, out=out)
+    assert y.data_ptr() == out.data_ptr()
+    assert np.array_equal(out.cpu().numpy().view(np.uint16), ref.view(np.uint16))
