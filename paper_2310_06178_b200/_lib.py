@@ -136,6 +136,16 @@ def require_device():
     return t.device("cuda", t.cuda.current_device())
 
 
+def current_stream_handle(dev) -> int:
+    """Raw cudaStream_t of the current stream on `dev` (an int).  Uses torch's
+    raw-stream query when available (~10x cheaper than building a Stream)."""
+    t = torch()
+    get_raw = getattr(t._C, "_cuda_getCurrentRawStream", None)
+    if get_raw is not None:
+        return int(get_raw(dev.index))
+    return int(t.cuda.current_stream(dev).cuda_stream)
+
+
 def stream_ptr():
     return ctypes.c_void_p(torch().cuda.current_stream().cuda_stream)
 

@@ -1174,11 +1174,12 @@ int msg_gemm(const uint8_t* packed, const uint8_t* wrep, int64_t m, int64_t k, i
   if (int e = validate_gemm(m, k, width, x_dtype, b, d, scale_mode, group_size)) return e;
   if (dtype_size(y_dtype) == 0) return fail(MSG_ERR_UNSUPPORTED, "bad output dtype %d", y_dtype);
   cudaStream_t s = as_stream(stream);
-  CodebookParam cb = make_codebook(values, width);
   FusedPlan p = fused_plan(m, k, width, values, x_dtype, b, d, scale_mode, group_size, flags);
-  if (!p.ok)
+  if (!p.ok) {
+    const CodebookParam cb = make_codebook(values, width);  // 2 KiB block: generic path only
     return run_generic(packed, m, k, width, cb, x, x_dtype, b, d, scale_mode, group_size, q,
                        q_dtype, y, y_dtype, workspace, ws_bytes, s);
+  }
   if (!wrep) return fail(MSG_ERR_VALUE, "fused path needs the repacked (quad) weight layout");
   if (ws_bytes < p.partial_bytes)
     return fail(MSG_ERR_WORKSPACE, "workspace too small: need %lld bytes",

@@ -124,7 +124,7 @@ def msgemm(pwm: PackedWeightMatrix, X, d: int, budget: int = DEFAULT_BUDGET,
     x_code = _lib.dtype_code(Xm.dtype)
     is_tensor = _lib.is_torch(X)
     on_device = is_tensor and X.is_cuda
-    stream = t.cuda.current_stream(dev)
+    stream = _lib.current_stream_handle(dev)
     call = _call_plan(pwm, dev, stream, b, x_code, Xm.dtype, d, table_dtype, symmetric,
                       out_dtype, int(_flags))
     y_dt = call.y_dtype
@@ -204,7 +204,7 @@ class _CallPlan:
         self._args_mid = (x_code, b, d, scale_mode, group_size, _lib.ptr(qd), q_code)
         self._ws = (ws, _lib.ptr(ws), ws.numel())
         self._flags = flags
-        self._stream = _lib.ctypes.c_void_p(stream.cuda_stream)
+        self._stream = _lib.ctypes.c_void_p(stream)
         self._keep = (wrep, qd)
         self._xs = self._xh = self._ys = self._yh = None
         self._fn = lib.msg_gemm
@@ -252,7 +252,7 @@ class _CallPlan:
 def _call_plan(pwm, dev, stream, b, x_code, x_dtype, d, table_dtype, symmetric, out_dtype,
                flags) -> _CallPlan:
     cache = pwm._device_cache
-    key = ("call", dev.index, stream.cuda_stream, b, x_code, d,
+    key = ("call", dev.index, stream, b, x_code, d,
            None if table_dtype is None else np.dtype(table_dtype).str, bool(symmetric),
            None if out_dtype is None else np.dtype(out_dtype).str, flags)
     plan = cache.get(key)
