@@ -88,3 +88,25 @@ def test_per_group_unaligned_falls_back_and_matches():
     assert _plan_layout(pwm, d, b, _lib.F32) == _lib.LAYOUT_NONE
     y = mg.msgemm(pwm, X, d)
     assert orc.rel_error(y, Wd, X) <= 1e-5
+
+
+@pytest.mark.parametrize("m,k,b", [(256, 8192 + 2, 4), (256, 8192 + 2, 8), (300, 4097, 12),
+                                   (100, 3000, 6), (4096, 2048, 16)])
+@pytest.mark.parametrize("per_row", [False, True])
+def test_row_block_finish_paths(m, k, b, per_row):
+    """Small m over long k gives many k-slices: the float4 finish with slice
+    groups (b % 4 == 0), the plain float4 finish and the scalar slice-group
+    finish (b % 4 != 0) -- each against the oracle, tails and per-row scales
+    included, and bitwise repeatable."""
+    rng = np.random.default_rng(m + k + b)
+    codes = rng.integers(0, 16, (m, k), dtype=np.uint8)
+    q = rng.uniform(0.5, 2.0, m).astype(np.float32) if per_row else None
+    pwm = mg.from_codes(codes, mg.int4_codebook(), scales=mg.PerRow(q=q) if per_row else None)
+    X = rng.standard_normal((k, b)).astype(np.float16)
+    y1 = mg.msgemm(pwm, X, 3)
+    y2 = mg.msgemm(pwm, X, 3)
+    assert np.array_equal(y1.view(np.uint16), y2.view(np.uint16))
+    W = orc.dense(pwm.data, k, 4, orc.int4_values()).astype(np.float64)
+    if per_row:
+        W = W * q[:, None].astype(np.float64)
+    assert orc.rel_error(y1, W, X) <= 2e-3
