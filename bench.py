@@ -397,24 +397,33 @@ def main():
     value = ops / (ms_step * 1e-3) / 1e9
     peaks = load_peaks()
     shard_cfg = type(cfg)(cfg.name, mr, kr, cfg.b, cfg.d, cfg.x_dtype, cfg.seed)
-    y_item = 4 if exact else 2
-    bytes_launch = algorithmic_bytes(shard_cfg, x_itemsize=2, y_itemsize=y_item)
+    x_item = Xh.dtype.itemsize                      # fp16 (or fp32 for config 1)
+    f32_tables = exact or x_item == 4
+    y_item = 4 if f32_tables else 2
+    lane = cfg.b == 1 and cfg.d == 3 and not f32_tables
+    bytes_launch = algorithmic_bytes(shard_cfg, x_itemsize=x_item, y_itemsize=y_item)
     achieved = bytes_launch / (ms_lut * 1e-3) / 1e9
     traffic = None
     tp = ROOT / "profiles" / "traffic.json"
     if tp.exists():
         traffic = json.loads(tp.read_text()).get(f"{cfg.name}@{world}")
     nb = kr // cfg.d
-    smem_bytes = (mr * nb + 2048 * nb) * cfg.b * 2          # LUT reads + half-table writes (fp16)
+    e_item = 4 if f32_tables else 2
+    smem_bytes = (mr * nb + 2048 * nb) * cfg.b * e_item     # LUT reads + half-table writes
     out = {
         "metric": "effective GOP/s (2*m*k*b/time) and achieved HBM GB/s vs roofline",
         "value": value, "unit": "GOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f16",
-        "data": "synthetic (seeded numpy default_rng; uniform int4 W, N(0,1) X)",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32" if x_item == 4 else "f16",
+        "data": "synthetic (seeded numpy default_rng; uniform int4 W, "
+                + ("integer X in [-127, 127]" if exact else "N(0,1) X") + ")",
         "config": {"workload": cfg.name, "m": cfg.m, "k": cfg.k, "b": cfg.b, "d": cfg.d,
-                   "x": "fp16", "tables": "fp16 sign-symmetric half tables (2048/group)",
-                   "accum": "f32", "y": "fp32" if exact else "fp16",
+                   "x": "fp32" if x_item == 4 else "fp16",
+                   "tables": ("fp32 sign-symmetric half tables" if f32_tables else
+                              "fp16 sign-symmetric half tables (2048/group"
+                              + (", 32 bank-private per chunk)" if lane else ")")),
+                   "accum": "int64 fixed point across CTAs" if lane else "f32",
+                   "y": "fp32" if f32_tables else "fp16",
                    "parallelism": (f"k-split x{world} + NCCL fp32 all-reduce" if ksplit else
                                    f"row-shard x{world}" + (" + NCCL all-gather" if world > 1 else "")),
                    "timing": "CUDA-graph replay of the K steps" if use_graphs else "eager launches",
@@ -422,7 +431,7 @@ def main():
                          f">= 3x L2) between steps"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
                      "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-                     "kernel": ("lane_lut_kernel" if (cfg.b == 1 and cfg.d == 3 and not exact)
+                     "kernel": ("lane_lut_kernel" if lane
                                 else "fused_lut_kernel"), "kernel_ms": ms_lut,
                      "kernel_share": ms_lut / ms_step, "algorithmic_bytes_per_launch": bytes_launch,
                      "peak_source": peaks["source"],
