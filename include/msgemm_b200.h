@@ -113,6 +113,22 @@ MSG_API int msg_encode_values(const double* weights, const double* grid, int64_t
                       int width, const double* values,
                       uint8_t* packed, int64_t* bad_count_and_first, void* stream);
 
+/* Conditioning of sign-symmetric tables per row (new; no reference
+ * counterpart -- the reference keeps full tables, lut.py:59-72).  ratio[i]
+ * (device float, m entries) = sqrt(sum_j (sum_{r<d} |v[c_jr]-beta|)^2) /
+ * sum_c |v[c_ic]| for width-4 rows: the expected half-table rounding error of
+ * row i relative to the reference's tolerance bound sum_c |W_ic||x_c|
+ * (suites.py:106-124) at unit activations; +inf for rows without a nonzero
+ * weight (they must come out exactly 0).  The Python layer computes rows
+ * above a dtype-dependent threshold with full tables instead. */
+MSG_API int msg_row_conditioning(const uint8_t* packed, int64_t m, int64_t k, int d,
+                                 const double* values, double beta, float* ratio, void* stream);
+
+/* Row gather / scatter of n rows of row_bytes bytes: scatter != 0 ->
+ * dst[idx[i]] = src[i]; else dst[i] = src[idx[i]].  idx: device int64 (n,). */
+MSG_API int msg_copy_rows(const void* src, const int64_t* idx, int64_t n, int64_t row_bytes,
+                          void* dst, int scatter, void* stream);
+
 /* ---------- phase 1 (lut.py) ---------- */
 
 /* Full table for one activation vector x (k,) with stride `ldx` elements:

@@ -33,7 +33,7 @@ EXPORTS = (
     "msg_unpack_codes", "msg_group_indices", "msg_encode_values", "msg_lut_build",
     "msg_repacked_bytes", "msg_repack", "msg_gemm_plan", "msg_gemm",
     "msg_dequant_mma_workspace_bytes", "msg_dequant_mma", "msg_set_tracing", "msg_read_trace",
-    "msg_mma_layout_bytes", "msg_repack_mma",
+    "msg_mma_layout_bytes", "msg_repack_mma", "msg_row_conditioning", "msg_copy_rows",
 )
 
 _c_i64 = ctypes.c_int64
@@ -60,6 +60,9 @@ _SIGS = {
                                  _vp, _c_i64, _vp]),
     "msg_mma_layout_bytes": (_c_i64, [_c_i64, _c_i64]),
     "msg_repack_mma": (_c_int, [_vp, _c_i64, _c_i64, _vp, _vp, _vp]),
+    "msg_row_conditioning": (_c_int, [_vp, _c_i64, _c_i64, _c_int, _vp, ctypes.c_double, _vp,
+                                      _vp]),
+    "msg_copy_rows": (_c_int, [_vp, _vp, _c_i64, _c_i64, _vp, _c_int, _vp]),
     "msg_set_tracing": (_c_int, [_c_int]),
     "msg_read_trace": (_c_int, [_vp, _c_int]),
 }
@@ -148,6 +151,16 @@ def current_stream_handle(dev) -> int:
 
 def stream_ptr():
     return ctypes.c_void_p(torch().cuda.current_stream().cuda_stream)
+
+
+def layout_ready() -> None:
+    """A cached weight layout was just written on the current stream: wait for
+    it once, so calls on any other stream (plans are per stream) never read a
+    partial layout.  Skipped while a CUDA graph is being captured (the capture
+    stream is the only stream then)."""
+    t = torch()
+    if not t.cuda.is_current_stream_capturing():
+        t.cuda.current_stream().synchronize()
 
 
 def ptr(t) -> ctypes.c_void_p:

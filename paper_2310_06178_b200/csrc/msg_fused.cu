@@ -1236,7 +1236,9 @@ int launch_finish(const float* partial, int S, int64_t m, int64_t b, int64_t k, 
   const int64_t total = m * b;
   // four outputs per thread group; slices split over SG groups when there are
   // few outputs per SM (e.g. 137 slices x 8192 x 4)
-  if (b % 4 == 0 && scale_mode != MSG_SCALE_PER_GROUP && S >= 2) {
+  // (float4 / uint2 stores of Y: a caller-supplied Y must be 16-byte aligned)
+  if (b % 4 == 0 && scale_mode != MSG_SCALE_PER_GROUP && S >= 2 &&
+      (reinterpret_cast<uintptr_t>(y) & 15) == 0) {
     int sg = 1;
     while (sg < 16 && 2 * sg <= S && (total / 4) * sg < (int64_t)sm_count() * 512) sg *= 2;
     const int opb = 256 / sg;

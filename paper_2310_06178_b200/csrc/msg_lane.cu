@@ -136,6 +136,7 @@ struct LaneParams {
   float beta;
   float fx_scale, fx_inv;  // 2^F, 2^-F: fixed-point grid of the cross-CTA reduction
   unsigned long long* acc;  // [m] int64 fixed-point row sums (zero between calls)
+  float* nonfin;            // [m] sums of non-finite chunk sums (zero between calls)
   const void* q;
   int q_dtype, scale_mode;
   void* y;
@@ -254,11 +255,17 @@ __device__ __forceinline__ void finish_pair(const LaneParams& P, int64_t row, co
   ulonglong2* ap = reinterpret_cast<ulonglong2*>(P.acc + row);
   const ulonglong2 raw = __ldcg(ap);
   __stcg(ap, make_ulonglong2(0ull, 0ull));
-  const float y0 = (__ll2float_rn((long long)raw.x) * P.fx_inv + f.add0) * f.q0;
-  store_as<float>(P.y, P.y_dtype, row, y0);
+  // a NaN / inf chunk sum (non-finite activations, or fp16 table overflow)
+  // cannot travel through the fixed-point sum: it was accumulated apart and
+  // replaces the row's finite part, as it would absorb it in a float sum
+  float2* np = reinterpret_cast<float2*>(P.nonfin + row);
+  const float2 nf = __ldcg(np);
+  if (nf.x != 0.f || nf.y != 0.f) __stcg(np, make_float2(0.f, 0.f));
+  const float s0 = nf.x != 0.f ? nf.x : __ll2float_rn((long long)raw.x) * P.fx_inv;
+  store_as<float>(P.y, P.y_dtype, row, (s0 + f.add0) * f.q0);
   if (row + 1 < P.m) {
-    const float y1 = (__ll2float_rn((long long)raw.y) * P.fx_inv + f.add1) * f.q1;
-    store_as<float>(P.y, P.y_dtype, row + 1, y1);
+    const float s1 = nf.y != 0.f ? nf.y : __ll2float_rn((long long)raw.y) * P.fx_inv;
+    store_as<float>(P.y, P.y_dtype, row + 1, (s1 + f.add1) * f.q1);
   }
 }
 
@@ -463,8 +470,11 @@ __global__ void __launch_bounds__(kLaneThreads, 1) lane_lut_kernel(LaneParams P)
 #pragma unroll
       for (int q = 0; q < TPW; ++q) {
         const int64_t row = row0 + q * 32;
-        const long long fx = __float2ll_rn((acc[q][0] + acc[q][1]) * P.fx_scale);
-        if (q < nv && row < P.m) red_add_u64(P.acc + row, fx);
+        const float cs = acc[q][0] + acc[q][1];
+        if (q < nv && row < P.m) {
+          if (isfinite(cs)) red_add_u64(P.acc + row, __float2ll_rn(cs * P.fx_scale));
+          else atomicAdd(P.nonfin + row, cs);
+        }
       }
     }
     seg_b = seg_e;
@@ -509,11 +519,11 @@ int lane_repack(const uint8_t* packed, int64_t m, int64_t k, uint8_t* out, cudaS
   return MSG_OK;
 }
 
-// workspace: [32 * ntiles] int64 accumulators (rows padded to whole tiles),
-// zero on entry and on exit
+// workspace: [32 * ntiles] int64 accumulators (rows padded to whole tiles)
+// then [32 * ntiles] float non-finite sums, zero on entry and on exit
 int64_t lane_workspace_bytes(int64_t m, int64_t k) {
   LaneLayout L = lane_layout(m, k);
-  return align256l(L.ntiles * 32 * 8);
+  return align256l(L.ntiles * 32 * 8) + align256l(L.ntiles * 32 * 4);
 }
 
 // Split the chunk-major tile sequence into `grid` contiguous CTA ranges that
@@ -632,6 +642,9 @@ int launch_lane(const uint8_t* wrep, int64_t m, int64_t k, const double* values,
   P.fx_scale = std::ldexp(1.0f, F);
   P.fx_inv = std::ldexp(1.0f, -F);
   P.acc = reinterpret_cast<unsigned long long*>(ws);
+  P.nonfin = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + align256l(L.ntiles * 32 * 8));
+  if ((reinterpret_cast<uintptr_t>(x) & 3) != 0)
+    return fail(MSG_ERR_VALUE, "the b=1 kernel needs 4-byte aligned activations");
   P.q = q;
   P.q_dtype = q_dtype;
   P.scale_mode = scale_mode;

@@ -6,6 +6,8 @@
 // nibble; width 2 -> column j in byte j/4 at bit 2*(j%4); other widths -> one
 // code per byte.  Group index (packing.py:201-228): first code least
 // significant, idx = sum_r code(j*d + r) << (width*r).
+#include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <mutex>
 
@@ -148,6 +150,59 @@ __global__ void encode_values_kernel(const double* __restrict__ w, const double*
   }
 }
 
+
+// ------------------------------------------------------- row conditioning
+// Sign-symmetric tables store H = sum_r (v[c_r] - beta) x_r, so a table
+// rounding error scales with sum_r |v - beta| |x_r| instead of the reference's
+// bound sum_r |v| |x_r| (suites.py:106-124).  ratio[i] is the expected
+// (random-walk) accumulated table error of row i relative to that bound, for
+// unit activations: sqrt(sum_j (sum_{r<d} |v[c_jr] - beta|)^2) / sum_c |v[c]|
+// (+inf for a row without a nonzero weight, which must come out exactly 0).
+// One warp per row, lanes stride over the d-groups.
+__global__ void row_conditioning_kernel(const uint8_t* __restrict__ packed, int64_t m, int64_t k,
+                                        int d, int rb, CodebookParam cb, double beta,
+                                        float* __restrict__ ratio) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nb = k / d;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < m;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const uint8_t* row = packed + i * rb;
+    double s2 = 0.0, wabs = 0.0;
+    for (int64_t j = lane; j < nb; j += 32) {
+      double sj = 0.0;
+      for (int r = 0; r < d; ++r) {
+        const double v = cb.v[code_at(row, j * d + r, 4)];
+        sj += fabs(v - beta);
+        wabs += fabs(v);
+      }
+      s2 += sj * sj;
+    }
+    for (int64_t j = nb * d + lane; j < k; j += 32) wabs += fabs(cb.v[code_at(row, j, 4)]);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      wabs += __shfl_xor_sync(0xffffffffu, wabs, o);
+    }
+    if (lane == 0) ratio[i] = wabs > 0.0 ? (float)(sqrt(s2) / wabs) : INFINITY;
+  }
+}
+
+// ------------------------------------------------------------- row copies
+// dst[idx[i]] = src[i] (scatter) or dst[i] = src[idx[i]] (gather), rows of
+// row_bytes bytes; 4-byte words when rows and pointers allow it.
+template <typename W>
+__global__ void copy_rows_kernel(const W* __restrict__ src, const int64_t* __restrict__ idx,
+                                 int64_t n, int64_t row_words, W* __restrict__ dst, int scatter) {
+  const int64_t total = n * row_words;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / row_words, w = t - i * row_words;
+    const int64_t r = idx[i];
+    if (scatter) dst[r * row_words + w] = src[i * row_words + w];
+    else dst[i * row_words + w] = src[r * row_words + w];
+  }
+}
+
 static int grid_for(int64_t n) {
   int64_t g = ceil_div(n, 256);
   int64_t cap = (int64_t)sm_count() * 16;
@@ -238,6 +293,37 @@ int msg_encode_values(const double* weights, const double* grid, int64_t m, int6
   CodebookParam cb = make_codebook(values, width);
   encode_values_kernel<<<grid_for(n), 256, 0, s>>>(weights, grid, m, k, width, cb, rb, packed,
                                                    reinterpret_cast<unsigned long long*>(bad));
+  MSG_LAUNCH_CHECK();
+  return MSG_OK;
+}
+
+int msg_row_conditioning(const uint8_t* packed, int64_t m, int64_t k, int d, const double* values,
+                         double beta, float* ratio, void* stream) {
+  if (d < 1) return fail(MSG_ERR_VALUE, "depth d must be >= 1");
+  if (m < 0 || k < 0) return fail(MSG_ERR_VALUE, "matrix dimensions must be non-negative");
+  if (m == 0) return MSG_OK;
+  CodebookParam cb = make_codebook(values, 4);
+  const int grid = (int)std::min<int64_t>(ceil_div(m * 32, 256), (int64_t)sm_count() * 16);
+  row_conditioning_kernel<<<grid, 256, 0, as_stream(stream)>>>(packed, m, k, d, row_bytes(k, 4),
+                                                               cb, beta, ratio);
+  MSG_LAUNCH_CHECK();
+  return MSG_OK;
+}
+
+int msg_copy_rows(const void* src, const int64_t* idx, int64_t n, int64_t row_bytes_, void* dst,
+                  int scatter, void* stream) {
+  if (n < 0 || row_bytes_ < 0) return fail(MSG_ERR_VALUE, "negative row count or size");
+  if (n == 0 || row_bytes_ == 0) return MSG_OK;
+  cudaStream_t s = as_stream(stream);
+  const bool words = row_bytes_ % 4 == 0 && ((uintptr_t)src & 3) == 0 && ((uintptr_t)dst & 3) == 0;
+  if (words) {
+    const int64_t rw = row_bytes_ / 4;
+    copy_rows_kernel<uint32_t><<<grid_for(n * rw), 256, 0, s>>>(
+        static_cast<const uint32_t*>(src), idx, n, rw, static_cast<uint32_t*>(dst), scatter);
+  } else {
+    copy_rows_kernel<uint8_t><<<grid_for(n * row_bytes_), 256, 0, s>>>(
+        static_cast<const uint8_t*>(src), idx, n, row_bytes_, static_cast<uint8_t*>(dst), scatter);
+  }
   MSG_LAUNCH_CHECK();
   return MSG_OK;
 }

@@ -100,6 +100,7 @@ class PackedWeightMatrix:
             _lib.check(_lib.lib().msg_repack(
                 _lib.ptr(self.device_data(dev)), self.m, self.k, d, layout, symmetric,
                 _lib.ptr(out), _lib.stream_ptr()))
+            _lib.layout_ready()
             cache[key] = out
         return cache[key]
 
@@ -114,7 +115,66 @@ class PackedWeightMatrix:
             _lib.check(_lib.lib().msg_repack_mma(
                 _lib.ptr(self.device_data(dev)), self.m, self.k,
                 _lib.host_doubles(self.codebook.values), _lib.ptr(out), _lib.stream_ptr()))
+            _lib.layout_ready()
             cache[key] = out
+        return cache[key]
+
+    def symmetric_conditioning(self, dev, d: int, beta: float):
+        """Per-row conditioning ratio of the sign-symmetric tables (device
+        float32 (m,), built once; csrc msg_row_conditioning): the expected
+        half-table rounding error relative to the reference's tolerance bound
+        sum_c |W_ic||x_c| (suites.py:106-124) at unit activations, +inf for
+        rows without a nonzero weight."""
+        cache = self._device_cache
+        key = ("cond", dev.index, d, float(beta))
+        if key not in cache:
+            t = _lib.torch()
+            out = t.empty(max(self.m, 1), dtype=t.float32, device=dev)
+            _lib.check(_lib.lib().msg_row_conditioning(
+                _lib.ptr(self.device_data(dev)), self.m, self.k, d,
+                _lib.host_doubles(self.codebook.values), float(beta), _lib.ptr(out),
+                _lib.stream_ptr()))
+            cache[key] = out[: self.m]
+        return cache[key]
+
+    def ill_conditioned_rows(self, dev, d: int, beta: float, threshold: float):
+        """Device int64 indices of the rows whose symmetric-table error could
+        reach the tolerance (conditioning ratio above `threshold`), built once
+        per threshold.  One host sync, at weight-preparation time."""
+        cache = self._device_cache
+        key = ("illrows", dev.index, d, float(beta), float(threshold))
+        if key not in cache:
+            t = _lib.torch()
+            ratio = self.symmetric_conditioning(dev, d, beta)
+            cache[key] = t.nonzero(ratio > threshold).reshape(-1).to(t.int64)
+        return cache[key]
+
+    def row_subset(self, dev, rows) -> "PackedWeightMatrix":
+        """Device-resident matrix of the given rows (same k, codebook and the
+        matching scale rows), gathered by msg_copy_rows; cached per row set."""
+        cache = self._device_cache
+        key = ("subset", dev.index, rows.data_ptr(), int(rows.numel()))
+        if key not in cache:
+            t = _lib.torch()
+            n = int(rows.numel())
+            src = self.device_data(dev)
+            data = t.empty((n, src.shape[1]), dtype=t.uint8, device=dev)
+            _lib.check(_lib.lib().msg_copy_rows(_lib.ptr(src), _lib.ptr(rows), n, int(src.shape[1]),
+                                                _lib.ptr(data), 0, _lib.stream_ptr()))
+            scales = None
+            q = self.device_scales(dev)
+            if q is not None:
+                qd = q.contiguous()
+                per = qd.numel() // max(self.m, 1)
+                qs = t.empty((n, per) if qd.dim() == 2 else (n,), dtype=qd.dtype, device=dev)
+                _lib.check(_lib.lib().msg_copy_rows(_lib.ptr(qd), _lib.ptr(rows), n,
+                                                    per * qd.element_size(), _lib.ptr(qs), 0,
+                                                    _lib.stream_ptr()))
+                scales = (PerRow(q=qs) if isinstance(self.scales, PerRow)
+                          else PerGroup(group_size=self.scales.group_size, q=qs))
+            sub = PackedWeightMatrix(m=n, k=self.k, width=self.width, data=data,
+                                     codebook=self.codebook, scales=scales)
+            cache[key] = sub
         return cache[key]
 
     def device_scales(self, dev):
@@ -156,6 +216,11 @@ def scale_grid(scales: ScaleSpec, m: int, k: int):
 
 def _host(arr):
     return arr.detach().cpu().numpy() if _lib.is_torch(arr) else arr
+
+
+def _host_row(arr, i):
+    """Row i on the host (a device matrix copies only that row)."""
+    return arr[i].detach().cpu().numpy() if _lib.is_torch(arr) else arr[i]
 
 
 def from_codes(codes, cb: Codebook, scales: ScaleSpec = None) -> PackedWeightMatrix:
@@ -230,7 +295,7 @@ def unpack(pwm: PackedWeightMatrix, i: int, j: int):
     """Decoded value at (i, j), scale NOT applied (packing.py:177-188)."""
     if not (0 <= i < pwm.m and 0 <= j < pwm.k):
         raise IndexError(f"({i}, {j}) out of bounds for {pwm.m}x{pwm.k}")
-    row = _host(pwm.data)[i]
+    row = _host_row(pwm.data, i)
     if pwm.width == 4:
         code = (int(row[j // 2]) >> (4 * (j % 2))) & 0xF
     elif pwm.width == 2:
@@ -267,9 +332,9 @@ def group_index(pwm: PackedWeightMatrix, i: int, j: int, d: int) -> int:
     if not 0 <= j < pwm.k // d:
         raise IndexError(f"block {j} out of bounds for k={pwm.k}, d={d}")
     idx = 0
+    row = _host_row(pwm.data, i)
     for r in range(d):
         col = j * d + r
-        row = _host(pwm.data)[i]
         if pwm.width == 4:
             code = (int(row[col // 2]) >> (4 * (col % 2))) & 0xF
         elif pwm.width == 2:

@@ -184,6 +184,81 @@ def main():
     Xi = rs.integers(-127, 128, size=(4096, 1)).astype(np.int64)
     add_gemm_case(gb, ms, pwm, Xi, 3, "cfg2_int")
     gb.save(OUT / "gemm_cases.npz")
+    sparse_cases(ms)
+
+
+def special_rows(rs, n, k, d):
+    """Rows the sign-symmetric tables must not be trusted with: all-zero,
+    single nonzero (random, +1, -1), 99% / 90% zero, only code 8 (-8), zero
+    but for the k % d tail, two nonzeros in one group, all +1, one full group."""
+    rows = []
+    nb = k // d
+    for t in range(n):
+        r = np.zeros(k, dtype=np.uint8)
+        kind = t % 11
+        if kind == 1:
+            r[rs.integers(0, k)] = rs.integers(1, 16)
+        elif kind == 2:
+            r[rs.integers(0, k)] = 1
+        elif kind == 3:
+            r[rs.integers(0, k)] = 15
+        elif kind in (4, 5):
+            frac = 0.01 if kind == 4 else 0.10
+            mask = rs.random(k) < frac
+            r[mask] = rs.integers(1, 16, size=int(mask.sum()))
+        elif kind == 6:
+            r[:] = 8
+        elif kind == 7:
+            r[nb * d:] = rs.integers(1, 16, size=k - nb * d)
+        elif kind == 8:
+            j = int(rs.integers(0, nb)) * d
+            r[j] = rs.integers(1, 16)
+            r[j + d - 1] = rs.integers(1, 16)
+        elif kind == 9:
+            r[:] = 1
+        elif kind == 10:
+            j = int(rs.integers(0, nb)) * d
+            r[j:j + d] = rs.integers(1, 16, size=d)
+        rows.append(r)
+    return np.stack(rows)
+
+
+def sparse_cases(ms):
+    """Sparse / zero weight rows (round 2): the reference's bound
+    |dy| <= rtol * sum_j |W_ij||x_j| (suites.py:104-124) is 0 for an all-zero
+    row, whose all-zero index contributes exactly 0 (lut.py:59-72).
+    Matrices: a mostly dense one with a few special rows, one made only of
+    special rows, and a config-1-like d=2 one.  X is stored once per dtype at
+    b=16; the b=1/4/8 cases use its first columns (b=1 as a vector)."""
+    cb = ms.int4_codebook()
+    sb = Bank()
+    rs = np.random.default_rng(4242)
+    mats = []
+    dense = rs.integers(0, 16, size=(150, 8192), dtype=np.uint8)
+    mixed = np.concatenate([dense[:75], special_rows(rs, 10, 8192, 3), dense[75:]])
+    mats.append(("mixed", mixed, 3, (np.float16, np.float32)))
+    mats.append(("special", special_rows(rs, 24, 4096, 3), 3, (np.float16, np.float32)))
+    d1 = rs.integers(0, 16, size=(60, 1024), dtype=np.uint8)
+    mats.append(("cfg1like", np.concatenate([d1[:30], special_rows(rs, 4, 1024, 2), d1[30:]]),
+                 2, (np.float32,)))
+    for name, codes, d, dts in mats:
+        pwm = ms.from_codes(codes, cb)
+        k = codes.shape[1]
+        arrays = {"data": pwm.data}
+        for dt in dts:
+            X = rs.standard_normal((k, 16)).astype(dt)
+            arrays[f"X_{np.dtype(dt).name}"] = X
+            for b in (1, 4, 8, 16):
+                Xb = X[:, 0].copy() if b == 1 else np.ascontiguousarray(X[:, :b])
+                arrays[f"Y_{np.dtype(dt).name}_b{b}"] = ms.msgemm(pwm, Xb, d)
+        Xi = rs.integers(-127, 128, size=(k, 8)).astype(np.int64)
+        arrays["X_int"] = Xi
+        arrays["Y_int_b1"] = ms.msgemm(pwm, Xi[:, 0].copy(), d)
+        arrays["Y_int_b8"] = ms.msgemm(pwm, Xi, d)
+        sb.add("sparse", arrays, name=name, m=pwm.m, k=k, width=4, d=d,
+               dtypes=[np.dtype(dt).name for dt in dts],
+               values=[float(v) for v in cb.values])
+    sb.save(OUT / "sparse_cases.npz")
 
 
 if __name__ == "__main__":
