@@ -71,7 +71,7 @@ extern "C" {
 #define MSG_FLAG_LUT_PHASE_ONLY 8 /* measurement: launch only the fused LUT kernel (Y untouched;
                                      a LANE workspace keeps the sums and must be re-zeroed) */
 #define MSG_FLAG_NO_LANE      16  /* do not use the b=1 lane kernel (use the row-block kernel) */
-#define MSG_FLAG_PAIR         32  /* opt-in: double-buffered 2-group row-block kernel (slower on B200, kept for study) */
+#define MSG_FLAG_NO_ROWBLOCK  32  /* do not use the batched d=3 row-block kernel (use the generic fused kernel) */
 #define MSG_FLAG_STATIC_WEIGHTS 64 /* the repacked weights were not written by the kernel launched just
                                       before on this stream: the LUT kernel may start streaming them
                                       before that kernel completes (programmatic dependent launch) */
@@ -80,14 +80,12 @@ extern "C" {
 #define MSG_LAYOUT_NONE 0  /* reference row-major nibbles only      */
 #define MSG_LAYOUT_QUAD 1  /* quad planes for the fused LUT kernel  */
 #define MSG_LAYOUT_LANE 2  /* lane-rotated 32-group chunks for the b=1, d=3 GEMV kernel */
-#define MSG_LAYOUT_PAIR 3  /* quad planes, half-quad pair rotation (double-buffered kernel) */
+/* 3: retired */
+#define MSG_LAYOUT_RB4  4  /* row-block planes, rounds of 4 groups (b >= 8: 8-column tiles)  */
+#define MSG_LAYOUT_RB8  5  /* row-block planes, rounds of 8 groups (b = 4..7: 4-column tiles) */
+#define MSG_LAYOUT_RB16 6  /* row-block planes, rounds of 16 groups (b = 2, 3: 2-column tiles) */
 
 MSG_API const char* msg_last_error(void);
-/* diagnostics: per-CTA trace records {smid, t_start_ns, t_end_ns, units,
- * phase[4]} (8 x uint64 each) of the LUT kernels launched while tracing is on
- * (at most 4096, last launch) */
-MSG_API int msg_set_tracing(int on);
-MSG_API int msg_read_trace(uint64_t* host_records, int max_records);
 MSG_API int msg_version(void);
 MSG_API int msg_device_sm_count(void);
 
@@ -119,7 +117,8 @@ MSG_API int msg_encode_values(const double* weights, const double* grid, int64_t
  * sum_c |v[c_ic]| for width-4 rows: the expected half-table rounding error of
  * row i relative to the reference's tolerance bound sum_c |W_ic||x_c|
  * (suites.py:106-124) at unit activations; +inf for rows without a nonzero
- * weight (they must come out exactly 0).  The Python layer computes rows
+ * weight (they must come out exactly 0) or with fewer than min(8, ceil(k/2))
+ * nonzero weights (their bound rests on a few |x_c|).  The Python layer computes rows
  * above a dtype-dependent threshold with full tables instead. */
 MSG_API int msg_row_conditioning(const uint8_t* packed, int64_t m, int64_t k, int d,
                                  const double* values, double beta, float* ratio, void* stream);

@@ -24,15 +24,16 @@ F32, F16, F64, I32, I64, U8, I8, I16, BF16 = range(9)
 SCALE_NONE, SCALE_PER_ROW, SCALE_PER_GROUP = 0, 1, 2
 FLAG_F32_ENTRIES, FLAG_NO_SYMMETRY, FLAG_FORCE_GENERIC, FLAG_LUT_PHASE_ONLY = 1, 2, 4, 8
 FLAG_NO_LANE = 16
-FLAG_PAIR = 32
+FLAG_NO_ROWBLOCK = 32
 FLAG_STATIC_WEIGHTS = 64
-LAYOUT_NONE, LAYOUT_QUAD, LAYOUT_LANE, LAYOUT_PAIR = 0, 1, 2, 3
+LAYOUT_NONE, LAYOUT_QUAD, LAYOUT_LANE = 0, 1, 2
+LAYOUT_RB4, LAYOUT_RB8, LAYOUT_RB16 = 4, 5, 6
 
 EXPORTS = (
     "msg_last_error", "msg_version", "msg_device_sm_count", "msg_pack_codes",
     "msg_unpack_codes", "msg_group_indices", "msg_encode_values", "msg_lut_build",
     "msg_repacked_bytes", "msg_repack", "msg_gemm_plan", "msg_gemm",
-    "msg_dequant_mma_workspace_bytes", "msg_dequant_mma", "msg_set_tracing", "msg_read_trace",
+    "msg_dequant_mma_workspace_bytes", "msg_dequant_mma",
     "msg_mma_layout_bytes", "msg_repack_mma", "msg_row_conditioning", "msg_copy_rows",
 )
 
@@ -63,8 +64,6 @@ _SIGS = {
     "msg_row_conditioning": (_c_int, [_vp, _c_i64, _c_i64, _c_int, _vp, ctypes.c_double, _vp,
                                       _vp]),
     "msg_copy_rows": (_c_int, [_vp, _vp, _c_i64, _c_i64, _vp, _c_int, _vp]),
-    "msg_set_tracing": (_c_int, [_c_int]),
-    "msg_read_trace": (_c_int, [_vp, _c_int]),
 }
 
 _lib = None
@@ -241,13 +240,3 @@ def reset_workspaces():
     for key, buf in _ws.items():
         if key[2] == "lane":
             buf.zero_()
-
-
-def read_trace(max_records: int = 4096):
-    """Per-CTA trace records (smid, t0_ns, t1_ns, units, phase0..3) of the last traced launch."""
-    buf = (ctypes.c_uint64 * (8 * max_records))()
-    n = lib().msg_read_trace(buf, max_records)
-    if n < 0:
-        check(n)
-    a = np.frombuffer(buf, dtype=np.uint64).reshape(max_records, 8)[:n]
-    return a[a[:, 2] > 0]

@@ -136,29 +136,7 @@ __device__ __forceinline__ void store_as(void* p, int dt, int64_t i, A v) {
 
 }  // namespace msg
 
-// ----------------------------------------------------------------------------
-// per-CTA tracing (msg_set_tracing / msg_read_trace): when enabled, kernels
-// record {smid, start globaltimer, end globaltimer, work units, 4 phase
-// timers} per CTA.
-// ----------------------------------------------------------------------------
 namespace msg {
-constexpr int kTraceMax = 4096;
-struct TraceRec {
-  unsigned long long smid, t0, t1, units;
-  unsigned long long ph[4];  // kernel-specific phase timers (ns)
-};
-TraceRec* trace_buffer();  // device pointer (nullptr when tracing is off)
-
-__device__ __forceinline__ unsigned long long global_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-__device__ __forceinline__ unsigned int sm_id() {
-  unsigned int r;
-  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
-  return r;
-}
 
 // ----------------------------------------------------------------------------
 // mbarrier + cp.async.bulk (TMA bulk copy) helpers

@@ -49,7 +49,22 @@ int64_t lane_workspace_bytes(int64_t m, int64_t k);
 int lane_repack(const uint8_t* packed, int64_t m, int64_t k, uint8_t* out, cudaStream_t s);
 int launch_lane(const uint8_t* wrep, int64_t m, int64_t k, const double* values, double beta,
                 const void* x, int scale_mode, const void* q, int q_dtype, void* y, int y_dtype,
-                void* ws, int64_t ws_bytes, bool early, int exp, cudaStream_t s);
+                void* ws, int64_t ws_bytes, bool early, bool lut_only, cudaStream_t s);
+// batched d = 3 row-block kernel (msg_rowblock.cu)
+struct TailVals;
+int rb_group_count(int64_t b);
+bool rb_eligible(int width, int x_dtype, int64_t b, int d, int scale_mode, bool sym,
+                 bool f32_entries, bool s_exact16);
+int64_t rb_layout_bytes(int64_t m, int64_t k, int G);
+int64_t rb_workspace_bytes(int64_t m, int64_t k, int64_t b);
+int rb_repack(const uint8_t* packed, int64_t m, int64_t k, int G, uint8_t* out, cudaStream_t s);
+int launch_rb(const uint8_t* wrep, int64_t m, int64_t k, const double* values, double beta,
+              const void* x, int64_t b, int scale_mode, const void* q, int q_dtype, void* y,
+              int y_dtype, void* ws, int64_t ws_bytes, bool early, bool lut_only,
+              const TailVals& tv, cudaStream_t s);
+static int rb_layout_groups(int layout) {
+  return layout == MSG_LAYOUT_RB4 ? 4 : layout == MSG_LAYOUT_RB8 ? 8 : layout == MSG_LAYOUT_RB16 ? 16 : 0;
+}
 
 static inline int64_t align256(int64_t v) { return (v + 255) / 256 * 256; }
 
@@ -85,7 +100,7 @@ __device__ __forceinline__ uint32_t nib(const uint8_t* row, int64_t j) {
 
 // one thread per (quad, padded row): rows fastest so plane stores coalesce
 __global__ void repack_quad_kernel(const uint8_t* __restrict__ packed, int64_t m, int64_t k,
-                                   int d, int rb, int symmetric, int rot, QuadLayout L,
+                                   int d, int rb, int symmetric, QuadLayout L,
                                    uint8_t* __restrict__ out) {
   const int64_t total = L.nq * L.mp;
   const int bits = 4 * d;
@@ -98,10 +113,9 @@ __global__ void repack_quad_kernel(const uint8_t* __restrict__ packed, int64_t m
     if (i < m) {
       const uint8_t* row = packed + i * rb;
       for (int g = 0; g < 4; ++g) {
-        // rot 4: position g of row i holds group (g + i) % 4 of the quad (a warp's
-        // lanes hit 4 different tables at every step); rot 2: each half-quad's
-        // two groups swap with the row parity (pair kernel)
-        const int gi = rot == 4 ? (int)((g + i) & 3) : (int)((g & 2) | ((g + i) & 1));
+        // position g of row i holds group (g + i) % 4 of the quad (a warp's
+        // lanes hit 4 different tables at every step)
+        const int gi = (int)((g + i) & 3);
         int64_t j = q * 4 + gi;
         uint32_t st = 0;
         if (j < L.nb) {
@@ -562,217 +576,6 @@ __global__ void __launch_bounds__(NT, 1) fused_lut_kernel(FusedParams P) {
 }
 
 // ============================================================================
-// double-buffered "pair" kernel: rounds of 2 groups, tables double-buffered so
-// one barrier per round separates gather(t) from build(t+1); warps that finish
-// their gather early start building the next tables, so LDS-heavy gathers and
-// STS/FMA-heavy builds interleave across warps instead of alternating for the
-// whole CTA.  K3 (PAIR layout) rotates each half-quad's two groups by row
-// parity, so a warp's lanes alternate between the two tables.
-// ============================================================================
-template <int EB> struct PairLayout {  // 2 groups per 128-byte row, 64 B each
-  static constexpr int SPG = 64 / EB;
-  static constexpr int LSPG = SPG == 2 ? 1 : SPG == 4 ? 2 : SPG == 8 ? 3 : SPG == 16 ? 4 : 5;
-  static constexpr int LEB = EB == 2 ? 1 : EB == 4 ? 2 : EB == 8 ? 3 : EB == 16 ? 4 : 5;
-  static __device__ __forceinline__ uint32_t off(uint32_t f, uint32_t gslot) {
-    return ((f >> LSPG) << 7) | ((f & (SPG - 1)) << LEB) | gslot;
-  }
-};
-
-template <int D, typename XT, typename ET, int BC, bool SYM, int RPT>
-__global__ void __launch_bounds__(kThreads, 1) pair_lut_kernel(FusedParams P) {
-  constexpr int ES = SYM ? (1 << (4 * D - 1)) : (1 << (4 * D));
-  constexpr int EB = BC * (int)sizeof(ET);
-  constexpr int LOWN = D == 1 ? 1 : (D == 2 ? 16 : 256);
-  constexpr int HIN = SYM ? 8 : 16;
-  constexpr int R = kThreads * RPT;
-  constexpr int LOB = FusedShape<D>::LOB, HIB = FusedShape<D>::HIB;
-  constexpr int PAIRB = 2 * ES * EB > 128 ? 2 * ES * EB : 128;
-  constexpr int XN = 2 * D * BC;  // staged activations per round
-  using TL = PairLayout<EB>;
-  extern __shared__ __align__(128) uint8_t smem[];
-
-  const int tid = threadIdx.x;
-  const int64_t row0 = (int64_t)blockIdx.x * R;
-  const int slice = blockIdx.y;
-  const int64_t c0 = (int64_t)blockIdx.z * BC;
-  const int64_t q_begin = (int64_t)slice * P.quads_per_slice;
-  const int64_t q_end = P.nq < q_begin + P.quads_per_slice ? P.nq : q_begin + P.quads_per_slice;
-  const int rows_valid = (int)((P.m - row0) < R ? (P.m - row0) : R);
-  const int rows_cp = (rows_valid + 7) & ~7;
-
-  uint8_t* tab = smem;                                         // [2][PAIRB]
-  uint8_t* stage = tab + 2 * PAIRB;                            // [2][R] lo, [2][R] hi
-  const size_t stage_bytes = (size_t)R * (LOB + HIB);
-  float* xs = reinterpret_cast<float*>(stage + 2 * stage_bytes);  // [2][XN]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(xs + 2 * XN);      // [2]
-
-  const uint8_t* lo_plane = P.wrep + P.lo_off;
-  const uint8_t* hi_plane = P.wrep + P.hi_off;
-  // rounds = pairs of groups; skip a trailing pair that holds no valid group
-  const int64_t g_lo = q_begin * 4;
-  const int64_t g_hi = (q_end * 4) < P.nb ? q_end * 4 : P.nb;
-  const int nrounds = g_hi > g_lo ? (int)((g_hi - g_lo + 1) / 2) : 0;
-
-  auto issue = [&](int64_t q) {  // TMA bulk copy of quad q's plane words (one thread)
-    const int buf = (int)((q - q_begin) & 1);
-    uint64_t* bar = bars + buf;
-    fence_proxy_async();
-    mbar_expect_tx(bar, (uint32_t)(rows_cp * (LOB + HIB)));
-    bulk_g2s(stage + (size_t)buf * R * LOB, lo_plane + (q * P.mp + row0) * LOB,
-             (uint32_t)(rows_cp * LOB), bar);
-    if constexpr (HIB > 0)
-      bulk_g2s(stage + 2 * (size_t)R * LOB + (size_t)buf * R * HIB,
-               hi_plane + (q * P.mp + row0) * HIB, (uint32_t)(rows_cp * HIB), bar);
-  };
-  // activations of round t: element e -> (group row gr = e / BC, column e % BC)
-  auto load_x = [&](int t) -> float {
-    float v = 0.f;
-    if (tid < XN && t < nrounds) {
-      const int c = tid % BC, gr = tid / BC;
-      const int64_t grow = (g_lo + 2 * (int64_t)t) * D + gr;  // k row
-      if (grow < P.nb * D && c0 + c < P.b) v = ldx<XT>(P.x, grow * P.b + c0 + c);
-    }
-    return v;
-  };
-  float sv[HIN];
-#pragma unroll
-  for (int h = 0; h < HIN; ++h) sv[h] = P.s[h];
-  float corr = 0.f;
-
-  auto build = [&](int t) {  // tables of round t into tab[t & 1]
-    const float* xr = xs + (t & 1) * XN;
-    uint8_t* dst = tab + (t & 1) * PAIRB;
-    if (SYM && tid < BC) {
-      float sacc = 0.f;
-#pragma unroll
-      for (int gr = 0; gr < 2 * D; ++gr) sacc += xr[gr * BC + tid];
-      corr += sacc;
-    }
-    for (int w = tid; w < 2 * LOWN; w += kThreads) {
-      const int g = w & 1, low = w >> 1;
-      const float* xg = xr + g * D * BC;
-      float base[BC];
-#pragma unroll
-      for (int c = 0; c < BC; ++c) {
-        float v = 0.f;
-        if constexpr (D >= 2) v = P.s[low & 15] * xg[c];
-        if constexpr (D >= 3) v = fmaf(P.s[(low >> 4) & 15], xg[BC + c], v);
-        base[c] = v;
-      }
-      float xtop[BC];
-#pragma unroll
-      for (int c = 0; c < BC; ++c) xtop[c] = xg[(D - 1) * BC + c];
-      const uint32_t gslot = (uint32_t)g << 6;
-#pragma unroll
-      for (int h = 0; h < HIN; ++h) {
-        float e[BC];
-        if constexpr (BC == 1) {
-          e[0] = fmaf(sv[h], xtop[0], base[0]);
-        } else {
-#pragma unroll
-          for (int c = 0; c < BC; c += 2)
-            fma2_to(e[c], e[c + 1], sv[h], xtop[c], xtop[c + 1], base[c], base[c + 1]);
-        }
-        store_entry<ET, BC>(dst + TL::off((uint32_t)(low + h * LOWN), gslot), e);
-      }
-    }
-  };
-
-  if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (tid == 0 && nrounds > 0) {
-    issue(q_begin);
-    if (q_begin + 1 < q_end) issue(q_begin + 1);
-  }
-  float xnext = 0.f;
-  if (tid < XN) {
-    xs[tid] = load_x(0);
-    xs[XN + tid] = load_x(1);
-  }
-  xnext = load_x(2);
-  __syncthreads();
-  if (nrounds > 0) build(0);
-  __syncthreads();
-
-  float acc[RPT][BC];
-#pragma unroll
-  for (int r = 0; r < RPT; ++r)
-#pragma unroll
-    for (int c = 0; c < BC; ++c) acc[r][c] = 0.f;
-  uint32_t gslot[2];  // table slice of position h's group for this lane (row parity)
-  gslot[0] = (uint32_t)(tid & 1) << 6;
-  gslot[1] = (uint32_t)((tid + 1) & 1) << 6;
-
-  for (int t = 0; t < nrounds; ++t) {
-    const int64_t pa = (g_lo >> 1) + t;  // global pair index
-    const int64_t q = pa >> 1;
-    const int hp = (int)(pa & 1);
-    const int qb = (int)((q - q_begin) & 1);
-    // quad q+1's words go into the buffer quad q-1 used (all its rounds are done)
-    if (tid == 0 && hp == 0 && q + 1 < q_end && q + 1 >= q_begin + 2) issue(q + 1);
-    if (hp == 0) mbar_wait(&bars[qb], (uint32_t)(((q - q_begin) >> 1) & 1));
-    // ---- gather round t
-    const uint8_t* lo_s = stage + (size_t)qb * R * LOB;
-    const uint16_t* hi_s = reinterpret_cast<const uint16_t*>(stage + 2 * (size_t)R * LOB +
-                                                             (size_t)qb * R * HIB);
-    const uint8_t* tq = tab + (t & 1) * PAIRB;
-#pragma unroll
-    for (int r = 0; r < RPT; ++r) {
-      const int li = r * kThreads + tid;
-      if (li < rows_valid) {
-        uint32_t lo, hi = 0;
-        if constexpr (LOB == 4) lo = reinterpret_cast<const uint32_t*>(lo_s)[li];
-        else lo = reinterpret_cast<const uint16_t*>(lo_s)[li];
-        if constexpr (HIB > 0) hi = hi_s[li];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t st = stored_index<D>(lo, hi, 2 * hp + h);
-          const uint32_t f = SYM ? (st & (ES - 1)) : st;
-          gather_acc<ET, BC, SYM, 4 * D - 1>(tq + TL::off(f, gslot[h]), st, acc[r]);
-        }
-      }
-    }
-    // ---- build round t+1 into the other buffer; stage x for round t+2
-    if (t + 1 < nrounds) build(t + 1);
-    if (tid < XN) xs[(t & 1) * XN + tid] = xnext;  // round t+2 (buffer of round t)
-    xnext = load_x(t + 3);
-    __syncthreads();
-  }
-  if constexpr (SYM) {
-    __syncthreads();
-    if (tid < BC) xs[tid] = P.beta * corr;
-    __syncthreads();
-    float cv[BC];
-#pragma unroll
-    for (int c = 0; c < BC; ++c) cv[c] = xs[c];
-#pragma unroll
-    for (int r = 0; r < RPT; ++r)
-#pragma unroll
-      for (int c = 0; c < BC; ++c) acc[r][c] += cv[c];
-  }
-#pragma unroll
-  for (int r = 0; r < RPT; ++r) {
-    const int li = r * kThreads + tid;
-    if (li < rows_valid) {
-      float* dst = P.partial + ((int64_t)slice * P.m + row0 + li) * P.b + c0;
-      if (c0 + BC <= P.b && BC >= 2 && (P.b % 2 == 0)) {
-#pragma unroll
-        for (int c = 0; c < BC; c += 2)
-          *reinterpret_cast<float2*>(dst + c) = make_float2(acc[r][c], acc[r][c + 1]);
-      } else {
-#pragma unroll
-        for (int c = 0; c < BC; ++c)
-          if (c0 + c < P.b) dst[c] = acc[r][c];
-      }
-    }
-  }
-}
-
-// ============================================================================
 // epilogue: deterministic slice reduction + tail + correction + per-row scale
 // ============================================================================
 struct TailVals {
@@ -937,7 +740,8 @@ __global__ void __launch_bounds__(256) finish_vec4_kernel(
 // host planning / dispatch
 // ============================================================================
 struct FusedPlan {
-  bool ok, lane, pair;
+  bool ok, lane, rb;
+  int rb_groups;
   int bc, rpt, ql, S, nrow_blocks, ncol_tiles, quads_per_slice;
   bool sym, f32_entries;
   int64_t smem, partial_bytes;
@@ -988,6 +792,19 @@ static FusedPlan fused_plan(int64_t m, int64_t k, int width, const double* value
     p.ok = true;
     return p;
   }
+  bool s_exact16 = true;
+  for (int c = 0; c < 16; ++c) {
+    const float sc = (float)(values[c] - beta);
+    if ((double)__half2float(__float2half_rn(sc)) != values[c] - beta) s_exact16 = false;
+  }
+  if (!(flags & MSG_FLAG_NO_ROWBLOCK) &&
+      rb_eligible(width, x_dtype, b, d, scale_mode, p.sym, p.f32_entries, s_exact16)) {
+    p.rb = true;
+    p.rb_groups = rb_group_count(b);
+    p.partial_bytes = rb_workspace_bytes(m, k, b);
+    p.ok = true;
+    return p;
+  }
   const int esize = p.f32_entries ? 4 : 2;
   const int64_t ES = p.sym ? (1 << (4 * d - 1)) : (1 << (4 * d));
   const int64_t budget = std::min<int64_t>(max_smem_optin(), 227 * 1024) - 2 * 1024;
@@ -1017,14 +834,6 @@ static FusedPlan fused_plan(int64_t m, int64_t k, int width, const double* value
   while (ql > 1 && ql * 4 * d * bc > 2 * kThreads) --ql;
   p.ql = (int)ql;
   p.smem = p.ql * quad_bytes(bc) + p.ql * 4 * d * bc * 4 + 16;  // + second activation buffer
-  // double-buffered pair kernel when two 2-group table buffers fit
-  const int64_t pairb = std::max<int64_t>(2 * ES * bc * esize, 128);
-  const int64_t pair_smem = 2 * pairb + 2 * (int64_t)kThreads * p.rpt * (lob + hib) +
-                            2 * (2 * d * bc) * 4 + 64;
-  if ((flags & MSG_FLAG_PAIR) && pair_smem <= budget) {
-    p.pair = true;
-    p.smem = pair_smem;
-  }
   p.partial_bytes = align256((int64_t)p.S * m * b * 4);
   p.ok = true;
   return p;
@@ -1040,26 +849,25 @@ template <int BC> constexpr int fused_nt() { return BC <= 4 ? 512 : kThreads; }
 template <int D, typename XT, typename ET, int BC, bool SYM, int RPT>
 static int launch_fused_t(const FusedPlan& pl, FusedParams& P, cudaStream_t s) {
   constexpr int NT = fused_nt<BC>();
-  auto kern = pl.pair ? pair_lut_kernel<D, XT, ET, BC, SYM, RPT>
-                      : fused_lut_kernel<D, XT, ET, BC, SYM, RPT * kThreads / NT, NT>;
-  static int configured_dev[2] = {-1, -1};  // one attribute call per kernel and device
+  auto kern = fused_lut_kernel<D, XT, ET, BC, SYM, RPT * kThreads / NT, NT>;
+  static int configured_dev = -1;  // one attribute call per kernel and device
   int dev = 0;
   cudaGetDevice(&dev);
-  if (configured_dev[pl.pair] != dev) {
+  if (configured_dev != dev) {
     MSG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         std::min(max_smem_optin(), 227 * 1024)));
-    configured_dev[pl.pair] = dev;
+    configured_dev = dev;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(pl.nrow_blocks, pl.S, pl.ncol_tiles);
-  cfg.blockDim = dim3(pl.pair ? kThreads : NT);
+  cfg.blockDim = dim3(NT);
   cfg.dynamicSmemBytes = pl.smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pl.pair ? 0 : 1;  // the pair kernel has no griddepcontrol
+  cfg.numAttrs = 1;
   MSG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, P));
   return MSG_OK;
 }
@@ -1104,7 +912,8 @@ extern "C" {
 int64_t msg_repacked_bytes(int64_t m, int64_t k, int d, int layout) {
   if (layout == MSG_LAYOUT_NONE) return 0;
   if (layout == MSG_LAYOUT_LANE) return d == 3 ? lane_layout_bytes(m, k) : -1;
-  if ((layout != MSG_LAYOUT_QUAD && layout != MSG_LAYOUT_PAIR) || d < 1 || d > 3) return -1;
+  if (rb_layout_groups(layout)) return d == 3 ? rb_layout_bytes(m, k, rb_layout_groups(layout)) : -1;
+  if (layout != MSG_LAYOUT_QUAD || d < 1 || d > 3) return -1;
   return quad_layout(m, k, d).total;
 }
 
@@ -1115,7 +924,12 @@ int msg_repack(const uint8_t* packed, int64_t m, int64_t k, int d, int layout, i
       return fail(MSG_ERR_UNSUPPORTED, "lane layout is for d=3 with an antisymmetric codebook");
     return lane_repack(packed, m, k, out, as_stream(stream));
   }
-  if (layout != MSG_LAYOUT_QUAD && layout != MSG_LAYOUT_PAIR)
+  if (rb_layout_groups(layout)) {
+    if (d != 3 || !symmetric)
+      return fail(MSG_ERR_UNSUPPORTED, "row-block layout is for d=3 with an antisymmetric codebook");
+    return rb_repack(packed, m, k, rb_layout_groups(layout), out, as_stream(stream));
+  }
+  if (layout != MSG_LAYOUT_QUAD)
     return fail(MSG_ERR_UNSUPPORTED, "unknown weight layout %d", layout);
   if (d < 1 || d > 3) return fail(MSG_ERR_UNSUPPORTED, "quad layout supports d in 1..3, got %d", d);
   QuadLayout L = quad_layout(m, k, d);
@@ -1123,9 +937,7 @@ int msg_repack(const uint8_t* packed, int64_t m, int64_t k, int d, int layout, i
   if (total == 0) return fail(MSG_ERR_UNSUPPORTED, "quad layout needs at least one full group");
   int grid = (int)std::min<int64_t>(ceil_div(total, 256), (int64_t)sm_count() * 16);
   repack_quad_kernel<<<grid, 256, 0, as_stream(stream)>>>(packed, m, k, d, row_bytes(k, 4),
-                                                         symmetric,
-                                                         layout == MSG_LAYOUT_PAIR ? 2 : 4, L,
-                                                         out);
+                                                         symmetric, L, out);
   MSG_LAUNCH_CHECK();
   return MSG_OK;
 }
@@ -1156,7 +968,10 @@ int msg_gemm_plan(int64_t m, int64_t k, int width, const double* values, int x_d
   if (int e = validate_gemm(m, k, width, x_dtype, b, d, scale_mode, group_size)) return e;
   FusedPlan p = fused_plan(m, k, width, values, x_dtype, b, d, scale_mode, group_size, flags);
   if (p.ok) {
-    *layout_out = p.lane ? MSG_LAYOUT_LANE : (p.pair ? MSG_LAYOUT_PAIR : MSG_LAYOUT_QUAD);
+    *layout_out = p.lane ? MSG_LAYOUT_LANE
+                : p.rb ? (p.rb_groups == 4 ? MSG_LAYOUT_RB4
+                                           : p.rb_groups == 8 ? MSG_LAYOUT_RB8 : MSG_LAYOUT_RB16)
+                       : MSG_LAYOUT_QUAD;
     *symmetric_out = p.sym ? 1 : 0;
     *ws_out = p.partial_bytes;
   } else {
@@ -1188,10 +1003,14 @@ int msg_gemm(const uint8_t* packed, const uint8_t* wrep, int64_t m, int64_t k, i
   if (p.sym) codebook_antisymmetric(values, 16, &beta);
   TailVals tv;
   for (int c = 0; c < 16; ++c) tv.v[c] = (float)values[c];
+  const bool early = (flags & MSG_FLAG_STATIC_WEIGHTS) != 0;
+  const bool lut_only = (flags & MSG_FLAG_LUT_PHASE_ONLY) != 0;
   if (p.lane)  // LUT_PHASE_ONLY: the LUT kernel alone (its sums stay in the workspace)
     return launch_lane(wrep, m, k, values, beta, x, scale_mode, q, q_dtype, y, y_dtype,
-                       workspace, ws_bytes, (flags & MSG_FLAG_STATIC_WEIGHTS) != 0,
-                       ((flags >> 16) & 0xFF) | ((flags & MSG_FLAG_LUT_PHASE_ONLY) ? 4 : 0), s);
+                       workspace, ws_bytes, early, lut_only, s);
+  if (p.rb)
+    return launch_rb(wrep, m, k, values, beta, x, b, scale_mode, q, q_dtype, y, y_dtype,
+                     workspace, ws_bytes, early, lut_only, tv, s);
   FusedParams P{};
   P.wrep = wrep;
   P.lo_off = p.L.lo_off;
@@ -1208,7 +1027,7 @@ int msg_gemm(const uint8_t* packed, const uint8_t* wrep, int64_t m, int64_t k, i
     if ((double)__half2float(__float2half_rn(P.s[c])) != values[c] - beta) P.s_exact16 = 0;
   }
   P.beta = (float)beta;
-  P.early = (flags & MSG_FLAG_STATIC_WEIGHTS) ? 1 : 0;
+  P.early = early ? 1 : 0;
   P.quads_per_slice = p.quads_per_slice;
   P.ql = p.ql;
   P.partial = reinterpret_cast<float*>(workspace);
@@ -1219,7 +1038,7 @@ int msg_gemm(const uint8_t* packed, const uint8_t* wrep, int64_t m, int64_t k, i
     case 3: e = launch_fused_d<3>(p, P, x_dtype, s); break;
   }
   if (e) return e;
-  if (flags & MSG_FLAG_LUT_PHASE_ONLY) return MSG_OK;
+  if (lut_only) return MSG_OK;
   const uint16_t* tailp =
       p.L.tail ? reinterpret_cast<const uint16_t*>(wrep + p.L.tail_off) : nullptr;
   return launch_finish(P.partial, p.S, m, b, k, d, tailp, tv, x, x_dtype, scale_mode, q, q_dtype,

@@ -141,10 +141,9 @@ struct LaneParams {
   int q_dtype, scale_mode;
   void* y;
   int y_dtype;
-  TraceRec* trace;  // per-CTA trace records or nullptr
   uint32_t ones;    // 0x3C003C00: two fp16 +1.0
   int early;        // MSG_FLAG_STATIC_WEIGHTS: stream weights before griddepcontrol.wait
-  int exp;          // 4: LUT kernel only (measurement); other bits: experiments
+  int lut_only;     // measurement: the LUT kernel alone (no finish kernel)
   int bounds[kMaxLaneCtas + 1];  // CTA c owns global tiles [bounds[c], bounds[c+1])
 };
 
@@ -307,13 +306,6 @@ __global__ void __launch_bounds__(kLaneThreads, 1) lane_lut_kernel(LaneParams P)
   if (tid == 0 && smem_u32(smem) != kSmemBase) __trap();  // the LDS immediate assumes it
   const int nt = P.ntiles;
   const int G0 = P.bounds[blockIdx.x], G1 = P.bounds[blockIdx.x + 1];  // G < 2^31
-  const unsigned long long t_start = P.trace ? global_ns() : 0ull;
-  unsigned long long t_build = 0, t_wait = 0, t_loop = 0, t_count = 0;  // trace phases
-
-  if (tid == 0 && P.trace) {
-    *reinterpret_cast<unsigned long long*>(corr_s + 100) = ~0ull;
-    *reinterpret_cast<unsigned long long*>(corr_s + 102) = 0ull;
-  }
   if (lane == 0)
     for (int i = 0; i < kSlots; ++i) mbar_init(&bars[i], 1);
   fence_mbar_init();
@@ -389,22 +381,10 @@ __global__ void __launch_bounds__(kLaneThreads, 1) lane_lut_kernel(LaneParams P)
     const int seg_e = min(G1, (c + 1) * nt);
     // ---- build chunk c's 32 bank-private half tables (groups beyond nb get
     // x = 0, i.e. all-zero tables, so padded positions contribute nothing)
-    if (P.trace && seg_b != G0) {  // earliest / latest warp arrival at the 2nd build
-      const unsigned long long ta = global_ns();
-      if (lane == 0) {
-        atomicMin(reinterpret_cast<unsigned long long*>(corr_s + 100), ta);
-        atomicMax(reinterpret_cast<unsigned long long*>(corr_s + 102), ta);
-      }
-    }
     asm volatile("cp.async.wait_group 1;" ::: "memory");  // chunk c landed (c+1 may be in flight)
     __syncthreads();
     const __half* xc = xbuf + (c & 1) * 96 + 3 * lane;
     const float x0 = __half2float(xc[0]), x1 = __half2float(xc[1]), x2 = __half2float(xc[2]);
-    const unsigned long long tb0 = P.trace ? global_ns() : 0ull;
-    if (P.trace && seg_b != G0) {
-      t_wait = *reinterpret_cast<unsigned long long*>(corr_s + 100);
-      t_count = *reinterpret_cast<unsigned long long*>(corr_s + 102);
-    }
     {
       if (warp == 0) {
         float sx = x0 + x1 + x2;
@@ -434,7 +414,6 @@ __global__ void __launch_bounds__(kLaneThreads, 1) lane_lut_kernel(LaneParams P)
       }
     }
     __syncthreads();
-    if (P.trace) t_build += global_ns() - tb0;
     const float corr = *corr_s;
     stage_x(c + 2);  // xbuf[c & 1] is free again: chunk c + 2 goes there
     int cb, ce;
@@ -478,14 +457,6 @@ __global__ void __launch_bounds__(kLaneThreads, 1) lane_lut_kernel(LaneParams P)
       }
     }
     seg_b = seg_e;
-  }
-  if (P.trace) t_loop = global_ns();
-  if (P.trace) {
-    __syncthreads();
-    if (tid == 0 && blockIdx.x < kTraceMax)
-      P.trace[blockIdx.x] =
-          TraceRec{sm_id(), t_start, global_ns(), (unsigned long long)(G1 - G0),
-                   {t_build, t_wait, t_loop, t_count}};
   }
 }
 
@@ -575,7 +546,7 @@ static int launch_lane_t(LaneParams& P, cudaStream_t s) {
   const int want = (int)std::max<int64_t>(1, std::min<int64_t>({G, sm_count(), kMaxLaneCtas}));
   // a second segment costs its table build (~10 tiles of lookups) plus the
   // barrier that waits for the slowest warp's last batch and the refilled
-  // ring: ~40 tiles measured at config 4 (tools/trace_cta.py)
+  // ring: ~40 tiles measured at config 4 (per-CTA timing traces, round 1)
   // the split depends only on the shape: computed once per (nchunk, ntiles,
   // grid) and reused (the bisection costs ~10 us of host time per call)
   struct BoundsKey { int64_t nchunk, nt; int grid; };
@@ -605,7 +576,7 @@ static int launch_lane_t(LaneParams& P, cudaStream_t s) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   MSG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, lane_lut_kernel<TPW>, P));
-  if (P.exp & 4) return MSG_OK;  // measurement: the LUT kernel alone
+  if (P.lut_only) return MSG_OK;  // measurement: the LUT kernel alone
   // the finishing kernel, queued with PDL behind the LUT kernel.  (An in-kernel
   // grid barrier instead measured 2 us slower per call: fence + arrival +
   // release round trips after the last CTA, vs. PDL's overlapped launch.)
@@ -618,7 +589,7 @@ static int launch_lane_t(LaneParams& P, cudaStream_t s) {
 
 int launch_lane(const uint8_t* wrep, int64_t m, int64_t k, const double* values, double beta,
                 const void* x, int scale_mode, const void* q, int q_dtype, void* y, int y_dtype,
-                void* ws, int64_t ws_bytes, bool early, int exp, cudaStream_t s) {
+                void* ws, int64_t ws_bytes, bool early, bool lut_only, cudaStream_t s) {
   LaneLayout L = lane_layout(m, k);
   if (ws_bytes < lane_workspace_bytes(m, k))
     return fail(MSG_ERR_WORKSPACE, "workspace too small: need %lld bytes",
@@ -650,14 +621,12 @@ int launch_lane(const uint8_t* wrep, int64_t m, int64_t k, const double* values,
   P.scale_mode = scale_mode;
   P.y = y;
   P.y_dtype = y_dtype;
-  P.trace = trace_buffer();
   P.ones = 0x3C003C00u;
   P.early = early ? 1 : 0;
-  P.exp = exp;
+  P.lut_only = lut_only ? 1 : 0;
   // One tile per warp batch: measured faster than 2-tile batches (whose ILP
   // is not needed with 16 warps) at configs 2 and 4 -- warps finish a segment
-  // within one tile of each other.  Experiment bit 16 selects 2-tile batches.
-  if (exp & 16) return launch_lane_t<2>(P, s);
+  // within one tile of each other.
   return launch_lane_t<1>(P, s);
 }
 

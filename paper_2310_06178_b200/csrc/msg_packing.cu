@@ -16,10 +16,6 @@
 namespace msg {
 
 static thread_local std::string g_last_error;
-static TraceRec* g_trace = nullptr;  // diagnostics: per-CTA trace records
-static bool g_trace_on = false;
-
-TraceRec* trace_buffer() { return g_trace_on ? g_trace : nullptr; }
 
 void set_error(const std::string& s) { g_last_error = s; }
 
@@ -157,7 +153,9 @@ __global__ void encode_values_kernel(const double* __restrict__ w, const double*
 // bound sum_r |v| |x_r| (suites.py:106-124).  ratio[i] is the expected
 // (random-walk) accumulated table error of row i relative to that bound, for
 // unit activations: sqrt(sum_j (sum_{r<d} |v[c_jr] - beta|)^2) / sum_c |v[c]|
-// (+inf for a row without a nonzero weight, which must come out exactly 0).
+// (+inf for a row without a nonzero weight, which must come out exactly 0,
+// and for a row with fewer than min(8, ceil(k/2)) nonzero weights: its bound
+// rests on a handful of |x_c|, any of which may be tiny).
 // One warp per row, lanes stride over the d-groups.
 __global__ void row_conditioning_kernel(const uint8_t* __restrict__ packed, int64_t m, int64_t k,
                                         int d, int rb, CodebookParam cb, double beta,
@@ -168,22 +166,30 @@ __global__ void row_conditioning_kernel(const uint8_t* __restrict__ packed, int6
        i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const uint8_t* row = packed + i * rb;
     double s2 = 0.0, wabs = 0.0;
+    int nnz = 0;
     for (int64_t j = lane; j < nb; j += 32) {
       double sj = 0.0;
       for (int r = 0; r < d; ++r) {
         const double v = cb.v[code_at(row, j * d + r, 4)];
         sj += fabs(v - beta);
         wabs += fabs(v);
+        nnz += v != 0.0;
       }
       s2 += sj * sj;
     }
-    for (int64_t j = nb * d + lane; j < k; j += 32) wabs += fabs(cb.v[code_at(row, j, 4)]);
+    for (int64_t j = nb * d + lane; j < k; j += 32) {
+      const double v = cb.v[code_at(row, j, 4)];
+      wabs += fabs(v);
+      nnz += v != 0.0;
+    }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) {
       s2 += __shfl_xor_sync(0xffffffffu, s2, o);
       wabs += __shfl_xor_sync(0xffffffffu, wabs, o);
+      nnz += __shfl_xor_sync(0xffffffffu, nnz, o);
     }
-    if (lane == 0) ratio[i] = wabs > 0.0 ? (float)(sqrt(s2) / wabs) : INFINITY;
+    const int64_t few = (k + 1) / 2 < 8 ? (k + 1) / 2 : 8;
+    if (lane == 0) ratio[i] = (wabs > 0.0 && nnz >= few) ? (float)(sqrt(s2) / wabs) : INFINITY;
   }
 }
 
@@ -225,23 +231,6 @@ const char* msg_last_error(void) { return g_last_error.c_str(); }
 int msg_version(void) { return 100; }
 
 int msg_device_sm_count(void) { return sm_count(); }
-
-int msg_set_tracing(int on) {
-  g_trace_on = on != 0;
-  if (g_trace_on && !g_trace) {
-    MSG_CUDA_CHECK(cudaMalloc(&g_trace, sizeof(TraceRec) * kTraceMax));  // diagnostics only
-  }
-  if (g_trace_on) MSG_CUDA_CHECK(cudaMemset(g_trace, 0, sizeof(TraceRec) * kTraceMax));
-  return MSG_OK;
-}
-
-int msg_read_trace(uint64_t* host, int max_records) {
-  if (!g_trace) return 0;
-  int n = max_records < kTraceMax ? max_records : kTraceMax;
-  MSG_CUDA_CHECK(cudaDeviceSynchronize());
-  MSG_CUDA_CHECK(cudaMemcpy(host, g_trace, sizeof(TraceRec) * n, cudaMemcpyDeviceToHost));
-  return n;
-}
 
 int msg_pack_codes(const uint8_t* codes, int64_t m, int64_t k, int width, uint8_t* packed,
                    void* stream) {

@@ -53,14 +53,25 @@ def _plan(m, k, b, d, dt=_lib.F16, flags=0, cb=None, scale=0, gs=0):
                                      (65536, 8192, 8, 3)])
 def test_plan_configs_take_fused_symmetric_path(m, k, b, d):
     st, lay, sym, ws = _plan(m, k, b, d)
-    want = _lib.LAYOUT_LANE if (b == 1 and d == 3) else _lib.LAYOUT_QUAD
+    if d != 3:
+        want = _lib.LAYOUT_QUAD
+    elif b == 1:
+        want = _lib.LAYOUT_LANE
+    else:   # batched d = 3: the row-block kernel, rounds of 32 / min(b, 8) groups
+        want = {8: _lib.LAYOUT_RB4, 16: _lib.LAYOUT_RB4, 256: _lib.LAYOUT_RB4}[b]
     assert st == 0 and lay == want and sym == 1 and ws > 0
-    # the row-block kernels remain selectable for the GEMV shapes
-    st, lay, sym, ws = _plan(m, k, b, d, flags=_lib.FLAG_NO_LANE)
+    # the generic fused kernel remains selectable for every shape
+    st, lay, sym, ws = _plan(m, k, b, d, flags=_lib.FLAG_NO_LANE | _lib.FLAG_NO_ROWBLOCK)
     assert st == 0 and lay == _lib.LAYOUT_QUAD
-    # the double-buffered pair kernel is opt-in
-    st, lay, sym, ws = _plan(m, k, b, d, flags=_lib.FLAG_NO_LANE | _lib.FLAG_PAIR)
-    assert st == 0 and lay == _lib.LAYOUT_PAIR
+
+
+@pytest.mark.parametrize("b,want", [(2, 6), (3, 6), (4, 5), (7, 5), (8, 4), (64, 4)])
+def test_plan_rowblock_round_width(b, want):
+    st, lay, sym, ws = _plan(8192, 8192, b, 3)
+    assert st == 0 and lay == want
+    assert _plan(8192, 8192, b, 3, dt=_lib.F32)[1] == _lib.LAYOUT_QUAD     # fp32 X: fp32 tables
+    assert _plan(8192, 8192, b, 3, flags=_lib.FLAG_F32_ENTRIES)[1] == _lib.LAYOUT_QUAD
+    assert _plan(8192, 8192, b, 3, flags=_lib.FLAG_NO_SYMMETRY)[1] == _lib.LAYOUT_QUAD
 
 
 def test_plan_routes_to_generic():

@@ -57,7 +57,7 @@ def check_close(y, W, X, Yref, tag):
 
 
 @pytest.mark.parametrize("i", range(len(GEMM)))
-@pytest.mark.parametrize("variant", ["default", "nosym", "generic", "f32tab", "nolane", "pair"])
+@pytest.mark.parametrize("variant", ["default", "nosym", "generic", "f32tab", "nolane", "norb"])
 def test_msgemm_matches_reference_golden(i, variant):
     meta, a = GEMM[i]
     pwm = _pwm(meta, a)
@@ -66,11 +66,11 @@ def test_msgemm_matches_reference_golden(i, variant):
         kw["symmetric"] = False
     if variant == "f32tab":
         kw["table_dtype"] = np.float32
-    if variant in ("generic", "nolane", "pair"):
+    if variant in ("generic", "nolane", "norb"):
         from paper_2310_06178_b200 import _lib
         # force the global-memory table path / the row-block kernels via C-ABI flags
         flag = {"generic": _lib.FLAG_FORCE_GENERIC, "nolane": _lib.FLAG_NO_LANE,
-                "pair": _lib.FLAG_NO_LANE | _lib.FLAG_PAIR}[variant]
+                "norb": _lib.FLAG_NO_LANE | _lib.FLAG_NO_ROWBLOCK}[variant]
         y = _run_flags(pwm, a["X"], meta["d"], flag)
     else:
         y = mg.msgemm(pwm, a["X"], meta["d"], **kw)

@@ -118,9 +118,9 @@ def _ratio_numpy(codes, d, beta):
     nb = k // d
     sj = np.abs(v[:, :nb * d] - beta).reshape(codes.shape[0], nb, d).sum(axis=2)
     wabs = np.abs(v).sum(axis=1)
-    with np.errstate(divide="ignore"):
-        return np.where(wabs > 0, np.sqrt((sj ** 2).sum(axis=1)) / np.where(wabs > 0, wabs, 1),
-                        np.inf)
+    nnz = (v != 0).sum(axis=1)
+    ok = (wabs > 0) & (nnz >= min(8, (k + 1) // 2))
+    return np.where(ok, np.sqrt((sj ** 2).sum(axis=1)) / np.where(ok, wabs, 1), np.inf)
 
 
 @pytest.mark.parametrize("name", ["mixed", "special", "cfg1like"])
