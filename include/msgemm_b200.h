@@ -180,6 +180,16 @@ MSG_API int msg_dequant_mma(const uint8_t* wmma, int64_t m, int64_t k, const dou
                             const void* x, int x_dtype, int64_t b, void* y, int y_dtype,
                             void* workspace, int64_t workspace_bytes, void* stream);
 
+/* ---------- dense reference product (gemm.py:206-216 naive_gemm) ---------- */
+/* Y (m,b) = W (m,k) @ X (k,b), operands of any supported dtype, converted
+ * in-kernel.  mode 0: both integer -> int64 Y, wrapping int64 arithmetic
+ * (numpy's int64 matmul); 1: fp16 Y, fp32 sum of exact products in k order
+ * (numpy's half loop, bit-exact); 2: f32 Y, 3: f64 Y, both from a fp64 sum in
+ * k order (numpy uses BLAS there: same values within rounding).  The Python
+ * layer picks the mode from np.result_type(W, X) like numpy does. */
+MSG_API int msg_naive_gemm(const void* w, int w_dtype, const void* x, int x_dtype, int64_t m,
+                           int64_t k, int64_t b, int mode, void* y, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

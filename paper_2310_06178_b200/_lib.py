@@ -35,6 +35,7 @@ EXPORTS = (
     "msg_repacked_bytes", "msg_repack", "msg_gemm_plan", "msg_gemm",
     "msg_dequant_mma_workspace_bytes", "msg_dequant_mma",
     "msg_mma_layout_bytes", "msg_repack_mma", "msg_row_conditioning", "msg_copy_rows",
+    "msg_naive_gemm",
 )
 
 _c_i64 = ctypes.c_int64
@@ -64,6 +65,8 @@ _SIGS = {
     "msg_row_conditioning": (_c_int, [_vp, _c_i64, _c_i64, _c_int, _vp, ctypes.c_double, _vp,
                                       _vp]),
     "msg_copy_rows": (_c_int, [_vp, _vp, _c_i64, _c_i64, _vp, _c_int, _vp]),
+    "msg_naive_gemm": (_c_int, [_vp, _c_int, _vp, _c_int, _c_i64, _c_i64, _c_i64, _c_int, _vp,
+                                _vp]),
 }
 
 _lib = None

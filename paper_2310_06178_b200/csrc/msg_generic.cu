@@ -311,3 +311,118 @@ extern "C" int msg_lut_build(const void* x, int dtype, int64_t k, int64_t ldx, i
   return lut_dispatch(dtype, x, ldx, 0, 1, block_lo, block_hi - block_lo, d, cb, entries,
                       as_stream(stream));
 }
+
+// ------------------------------------------------------------------ naive_gemm
+// Dense reference product Y = W @ X (gemm.py:206-216) with numpy's
+// semantics: both operands integer -> int64 products and sums (two's
+// complement wrap, order-free); otherwise both operands are converted to the
+// result dtype numpy picks (np.result_type) and multiplied:
+//   f16: numpy's non-BLAS half loop -- fp32 sum over k in order of exact fp32
+//        products, rounded to fp16 once (bit-exact against numpy);
+//   f32 / f64: BLAS in numpy (order unspecified); here a correctly rounded
+//        fp64 sum in k order, rounded to the result dtype.
+// Tiles of 64 rows x 16 columns x 32 k staged through shared memory (coalesced
+// row-major loads of W and X); each thread owns 4 rows of one column and walks
+// k in order, so the summation order is fixed whatever the tiling.
+namespace msg {
+
+enum NaiveMode { NAIVE_INT = 0, NAIVE_F16 = 1, NAIVE_F32 = 2, NAIVE_F64 = 3 };
+
+template <int MODE> struct NaiveT;
+template <> struct NaiveT<NAIVE_INT> {
+  using V = int64_t; using A = uint64_t;
+  static __device__ __forceinline__ V load(const void* p, int dt, int64_t i) { return load_as<int64_t>(p, dt, i); }
+  static __device__ __forceinline__ A step(A acc, V a, V b) { return acc + (uint64_t)a * (uint64_t)b; }
+  static __device__ __forceinline__ void store(void* p, int dt, int64_t i, A acc) { ((int64_t*)p)[i] = (int64_t)acc; }
+};
+template <> struct NaiveT<NAIVE_F16> {
+  using V = float; using A = float;   // operands hold fp16-rounded values
+  static __device__ __forceinline__ V load(const void* p, int dt, int64_t i) {
+    return dt == MSG_F16 ? __half2float(((const __half*)p)[i])
+                         : __half2float(__double2half(load_as<double>(p, dt, i)));
+  }
+  static __device__ __forceinline__ A step(A acc, V a, V b) { return __fadd_rn(acc, __fmul_rn(a, b)); }
+  static __device__ __forceinline__ void store(void* p, int, int64_t i, A acc) { ((__half*)p)[i] = __float2half_rn(acc); }
+};
+template <> struct NaiveT<NAIVE_F32> {
+  using V = float; using A = double;
+  static __device__ __forceinline__ V load(const void* p, int dt, int64_t i) {
+    return dt == MSG_F32 ? ((const float*)p)[i] : (float)load_as<double>(p, dt, i);
+  }
+  static __device__ __forceinline__ A step(A acc, V a, V b) { return fma((double)a, (double)b, acc); }
+  static __device__ __forceinline__ void store(void* p, int, int64_t i, A acc) { ((float*)p)[i] = (float)acc; }
+};
+template <> struct NaiveT<NAIVE_F64> {
+  using V = double; using A = double;
+  static __device__ __forceinline__ V load(const void* p, int dt, int64_t i) { return load_as<double>(p, dt, i); }
+  static __device__ __forceinline__ A step(A acc, V a, V b) { return fma(a, b, acc); }
+  static __device__ __forceinline__ void store(void* p, int, int64_t i, A acc) { ((double*)p)[i] = acc; }
+};
+
+constexpr int NV_BM = 64, NV_BN = 16, NV_BK = 32, NV_THREADS = 256;
+
+template <int MODE>
+__global__ void __launch_bounds__(NV_THREADS)
+naive_gemm_kernel(const void* __restrict__ W, int w_dt, const void* __restrict__ X, int x_dt,
+                  int64_t m, int64_t k, int64_t b, void* __restrict__ Y) {
+  using T = NaiveT<MODE>;
+  using V = typename T::V;
+  using A = typename T::A;
+  __shared__ V ws[NV_BM][NV_BK + 1];
+  __shared__ V xs[NV_BK][NV_BN];
+  const int tid = threadIdx.x;
+  const int col = tid % NV_BN, rq = tid / NV_BN;          // 16 row quads x 16 columns
+  const int64_t row0 = (int64_t)blockIdx.x * NV_BM, col0 = (int64_t)blockIdx.y * NV_BN;
+  A acc[4] = {A(0), A(0), A(0), A(0)};
+  for (int64_t k0 = 0; k0 < k; k0 += NV_BK) {
+    for (int e = tid; e < NV_BM * NV_BK; e += NV_THREADS) {
+      int r = e / NV_BK, c = e % NV_BK;
+      int64_t gr = row0 + r, gc = k0 + c;
+      ws[r][c] = (gr < m && gc < k) ? T::load(W, w_dt, gr * k + gc) : V(0);
+    }
+    for (int e = tid; e < NV_BK * NV_BN; e += NV_THREADS) {
+      int r = e / NV_BN, c = e % NV_BN;
+      int64_t gr = k0 + r, gc = col0 + c;
+      xs[r][c] = (gr < k && gc < b) ? T::load(X, x_dt, gr * b + gc) : V(0);
+    }
+    __syncthreads();
+    const int kk = (k - k0 < NV_BK) ? (int)(k - k0) : NV_BK;
+    for (int c = 0; c < kk; ++c) {
+      V xv = xs[c][col];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[i] = T::step(acc[i], ws[rq * 4 + i][c], xv);
+    }
+    __syncthreads();
+  }
+  const int64_t gc = col0 + col;
+  if (gc >= b) return;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int64_t gr = row0 + rq * 4 + i;
+    if (gr < m) T::store(Y, 0, gr * b + gc, acc[i]);
+  }
+}
+
+}  // namespace msg
+
+extern "C" int msg_naive_gemm(const void* w, int w_dtype, const void* x, int x_dtype, int64_t m,
+                              int64_t k, int64_t b, int mode, void* y, void* stream) {
+  if (m < 0 || k < 0 || b < 0) return fail(MSG_ERR_VALUE, "negative dimension");
+  if (dtype_size(w_dtype) <= 0 || dtype_size(x_dtype) <= 0 || w_dtype == MSG_BF16 || x_dtype == MSG_BF16)
+    return fail(MSG_ERR_UNSUPPORTED, "naive_gemm: unsupported operand dtype (%d, %d)", w_dtype, x_dtype);
+  if (m == 0 || b == 0) return MSG_OK;
+  if (mode == NAIVE_INT && !(dtype_is_int(w_dtype) && dtype_is_int(x_dtype)))
+    return fail(MSG_ERR_VALUE, "naive_gemm: integer mode needs integer operands");
+  dim3 grid((unsigned)ceil_div(m, NV_BM), (unsigned)ceil_div(b, NV_BN));
+  if (grid.y > 65535) return fail(MSG_ERR_UNSUPPORTED, "naive_gemm: b too large");
+  cudaStream_t s = as_stream(stream);
+  switch (mode) {
+    case NAIVE_INT: naive_gemm_kernel<NAIVE_INT><<<grid, NV_THREADS, 0, s>>>(w, w_dtype, x, x_dtype, m, k, b, y); break;
+    case NAIVE_F16: naive_gemm_kernel<NAIVE_F16><<<grid, NV_THREADS, 0, s>>>(w, w_dtype, x, x_dtype, m, k, b, y); break;
+    case NAIVE_F32: naive_gemm_kernel<NAIVE_F32><<<grid, NV_THREADS, 0, s>>>(w, w_dtype, x, x_dtype, m, k, b, y); break;
+    case NAIVE_F64: naive_gemm_kernel<NAIVE_F64><<<grid, NV_THREADS, 0, s>>>(w, w_dtype, x, x_dtype, m, k, b, y); break;
+    default: return fail(MSG_ERR_VALUE, "naive_gemm: bad mode %d", mode);
+  }
+  MSG_LAUNCH_CHECK();
+  return MSG_OK;
+}

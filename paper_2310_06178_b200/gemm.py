@@ -354,12 +354,17 @@ def msgemm_traced(pwm: PackedWeightMatrix, x, d: int, budget: int = DEFAULT_BUDG
     return y, trace
 
 
-def naive_gemm(W, X):
-    """Dense reference W @ X (gemm.py:206-216), on the GPU (cuBLAS via torch).
+_NAIVE_MODES = {np.dtype(np.float16): 1, np.dtype(np.float32): 2, np.dtype(np.float64): 3}
 
-    Integer inputs are accumulated exactly: in float64 when every partial sum
-    provably stays below 2^53, else the call refuses (NotImplementedError)
-    rather than round.
+
+def naive_gemm(W, X):
+    """Dense reference W @ X (gemm.py:206-216) on the GPU (``msg_naive_gemm``).
+
+    numpy's semantics: integer x integer -> int64 products and sums (wrapping,
+    bit-exact); otherwise both operands go to ``np.result_type(W, X)`` --
+    float16 sums exact products in fp32 in k order and rounds once (numpy's
+    half loop, bit-exact); float32/float64 sum in fp64 in k order (numpy calls
+    BLAS there; same values within rounding).
     """
     t = _lib.torch()
     on_device = _lib.is_torch(X) or _lib.is_torch(W)
@@ -367,19 +372,32 @@ def naive_gemm(W, X):
     Xm, was_vector = _as_matrix(X)
     if Wa.ndim != 2 or Wa.shape[1] != Xm.shape[0]:
         raise ValueError(f"shape mismatch: W {tuple(Wa.shape)} x X {tuple(Xm.shape)}")
-    dev = _lib.require_device()
-    wd, xd = _lib.to_device(Wa, dev), _lib.to_device(Xm, dev)
-    ints = not wd.is_floating_point() and not xd.is_floating_point()
-    if ints:
-        bound = (float(wd.abs().max()) if wd.numel() else 0.0) * \
-                (float(xd.abs().max()) if xd.numel() else 0.0) * max(int(wd.shape[1]), 1)
-        if bound >= 2.0 ** 53:
-            raise NotImplementedError("integer naive_gemm beyond exact float64 range")
-        Y = (wd.double() @ xd.double()).round().to(t.int64)
+    wdt, xdt = _np_dtype(Wa), _np_dtype(Xm)
+    wdt = None if wdt is None else np.dtype(wdt)
+    xdt = None if xdt is None else np.dtype(xdt)
+    if wdt is None or xdt is None or wdt.kind not in "iufb" or xdt.kind not in "iufb":
+        raise NotImplementedError(f"naive_gemm: dtypes {wdt}, {xdt} are not supported on the GPU")
+    if wdt.kind in "iub" and xdt.kind in "iub":
+        mode, res = 0, np.dtype(np.int64)
     else:
-        res = np.result_type(_np_dtype(wd) or np.float64, _np_dtype(xd) or np.float64)
-        ct = _lib.torch_dtype_of(res)
-        Y = wd.to(ct) @ xd.to(ct)
+        res = np.result_type(wdt, xdt)
+        if res not in _NAIVE_MODES:
+            raise NotImplementedError(f"naive_gemm: result dtype {res} is not supported on the GPU")
+        mode = _NAIVE_MODES[res]
+    dev = _lib.require_device()
+
+    def operand(a, dt):
+        if not _lib.is_torch(a) and (dt.kind == "b" or dt in (np.dtype(np.uint16), np.dtype(np.uint32),
+                                                               np.dtype(np.uint64))):
+            a = a.astype(np.uint8 if dt.kind == "b" else np.int64)   # same int64 wrap
+        return _lib.to_device(a, dev).contiguous()
+
+    wd, xd = operand(Wa, wdt), operand(Xm, xdt)
+    m, k, b = int(wd.shape[0]), int(wd.shape[1]), int(xd.shape[1])
+    Y = t.empty((m, b), dtype=_lib.torch_dtype_of(res), device=dev)
+    _lib.check(_lib.lib().msg_naive_gemm(_lib.ptr(wd), _lib.dtype_code(wd.dtype), _lib.ptr(xd),
+                                         _lib.dtype_code(xd.dtype), m, k, b, mode, _lib.ptr(Y),
+                                         _lib.stream_ptr()))
     if was_vector:
         Y = Y[:, 0]
     return Y if on_device else Y.cpu().numpy()

@@ -15,6 +15,7 @@ suites.py:47-49) -- no external dataset is involved.
 
 from __future__ import annotations
 
+import hashlib
 import json
 import sys
 import zlib
@@ -185,6 +186,7 @@ def main():
     add_gemm_case(gb, ms, pwm, Xi, 3, "cfg2_int")
     gb.save(OUT / "gemm_cases.npz")
     sparse_cases(ms)
+    casegen_digests(ms)
 
 
 def special_rows(rs, n, k, d):
@@ -261,5 +263,46 @@ def sparse_cases(ms):
     sb.save(OUT / "sparse_cases.npz")
 
 
+def casegen_digests(ms):
+    """Digests of the reference's own CaseGen draws (suites.py:27-85) for the
+    suites its tests run: acceptance criterion 1 (test_acceptance.py:50-61),
+    test_suites.py:6-38 and the formula suite.  They pin the restatement in
+    oracle/casegen.py, so the GPU replay of those suites runs the reference's
+    exact cases.  For the exact suites the digest of the reference msgemm
+    outputs is recorded too (int64, bit-exact)."""
+    sys.path.insert(0, str(OUT.parents[1]))
+    from oracle.casegen import Case
+    suites = {
+        "crit1_d1": (dict(seed=1001, depths=(1,)), 1000, {}),
+        "crit1_d2": (dict(seed=1002, depths=(2,)), 1000, {}),
+        "crit1_d3": (dict(seed=1003, depths=(3,)), 1000, {}),
+        "crit1_d4": (dict(seed=1004, depths=(4,)), 1000, {}),
+        "crit1_f32": (dict(seed=2000, mode="f32"), 1000, {}),
+        "suite_exact_small": (dict(seed=1), 100, {}),
+        "suite_f32_small": (dict(seed=2, mode="f32"), 100, {}),
+        "formula": (dict(seed=5), 50, dict(divisible_only=True, scale_mode="none")),
+    }
+    out = {}
+    for name, (kw, n, draw_kw) in suites.items():
+        gen = ms.suites.CaseGen(**kw)
+        hc, hy = hashlib.sha256(), hashlib.sha256()
+        for _ in range(n):
+            pwm, X, d, seed = gen.draw(**draw_kw)
+            mode, gs, q = scale_meta(pwm)
+            Case(seed, d, ms.packing.codes(pwm), X, mode, gs,
+                 None if mode == "none" else q).digest_update(hc)
+            if kw.get("mode", "exact") == "exact":
+                hy.update(np.ascontiguousarray(ms.msgemm(pwm, X, d)).tobytes())
+        out[name] = {"kwargs": {k: list(v) if isinstance(v, tuple) else v for k, v in kw.items()},
+                     "cases": n, "draw": draw_kw, "cases_sha256": hc.hexdigest(),
+                     "Y_sha256": hy.hexdigest() if kw.get("mode", "exact") == "exact" else None}
+    path = OUT / "casegen_digests.json"
+    path.write_text(json.dumps({"numpy_version": np.__version__, "suites": out}, indent=1) + "\n")
+    print(f"wrote {path}")
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["casegen"]:
+        casegen_digests(_ref())
+    else:
+        main()

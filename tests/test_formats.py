@@ -85,3 +85,11 @@ def test_load_weights_device_matches_host(tmp_path):
     y_dev = mg.msgemm(dev_pwm, torch.from_numpy(X).cuda(), 3).cpu().numpy()
     y_host = mg.msgemm(F.read_weights(p), X, 3)
     assert np.array_equal(y_dev.view(np.uint16), y_host.view(np.uint16))
+    # against the oracle on the file's own bytes (not a self-comparison)
+    W = orc.dense(data, k, 4, orc.int4_values())
+    assert np.array_equal(np.asarray(dev_pwm.data.cpu()), data)
+    assert orc.rel_error(y_dev, W, X) <= 2e-3
+    Xi = rng.integers(-127, 128, (k, 2)).astype(np.int64)
+    yi = mg.msgemm(dev_pwm, torch.from_numpy(Xi.astype(np.float16)).cuda(), 3,
+                   table_dtype=np.float32, out_dtype=np.float32).cpu().numpy()
+    assert np.array_equal(yi.astype(np.int64), orc.msgemm(data, m, k, 4, orc.int4_values(), Xi, 3))

@@ -122,3 +122,35 @@ def test_workers_invariant():
     a = orc.msgemm(data, 20, 30, 4, vals, X, 3)
     b = orc.msgemm(data, 20, 30, 4, vals, X, 3, workers=4)
     assert np.array_equal(a.view(np.uint16), b.view(np.uint16))
+
+
+# ---------------------------------------------------------------- CaseGen suites
+
+def _casegen_digests():
+    import json
+    from pathlib import Path
+    return json.loads((Path(__file__).parent / "golden" / "casegen_digests.json").read_text())["suites"]
+
+
+@pytest.mark.parametrize("name", ["crit1_d1", "crit1_d2", "crit1_d3", "crit1_d4", "crit1_f32",
+                                  "suite_exact_small", "suite_f32_small", "formula"])
+def test_casegen_reproduces_reference_cases(name):
+    """oracle/casegen.py draws the reference's own cases (suites.py:27-85),
+    and on the exact suites the oracle's msgemm returns the reference's bytes."""
+    import hashlib
+    from oracle.casegen import CaseGen
+    ent = _casegen_digests()[name]
+    kw = {k: tuple(v) if isinstance(v, list) else v for k, v in ent["kwargs"].items()}
+    gen = CaseGen(**kw)
+    hc, hy = hashlib.sha256(), hashlib.sha256()
+    for _ in range(ent["cases"]):
+        c = gen.draw(**ent["draw"])
+        c.digest_update(hc)
+        if ent["Y_sha256"] is not None:
+            y = orc.msgemm(orc.pack_rows(c.codes.astype(np.uint8), 4), c.m, c.k, 4, orc.int4_values(),
+                           c.X, c.d, None if c.scale_mode == "none" else c.scale_mode,
+                           c.group_size, c.q)
+            hy.update(np.ascontiguousarray(y).tobytes())
+    assert hc.hexdigest() == ent["cases_sha256"]
+    if ent["Y_sha256"] is not None:
+        assert hy.hexdigest() == ent["Y_sha256"]
