@@ -106,9 +106,9 @@ class ClockSampler(threading.Thread):
 
 # --------------------------------------------------------------------------- CPU baseline
 class CpuArm:
-    """The oracle port (numpy restatement of the reference's msgemm) on row
-    samples of the same workload, host threads across batch columns (the
-    reference's own ThreadPool split, gemm.py:136-152)."""
+    """The oracle port (numpy restatement of the reference's msgemm) on the same
+    workload, host threads across batch columns (the reference's own
+    ThreadPool split, gemm.py:136-152; workers=1 is the reference as shipped)."""
 
     def __init__(self, cfg):
         from oracle import msgemm_oracle as orc
@@ -117,54 +117,75 @@ class CpuArm:
         self.data = weights(cfg)
         X = activations(cfg)
         self.X = X.astype(np.int64) if cfg.x_dtype == "int" else X
-        self.cores = min(len(os.sched_getaffinity(0)), max(cfg.b, 1))
+        self.host_cores = len(os.sched_getaffinity(0))
+        self.cores = min(self.host_cores, max(cfg.b, 1))
         self.vals = orc.int4_values()
 
-    def run(self, r0, rows):
+    def run(self, r0, rows, workers=None):
         cfg = self.cfg
         r0 = r0 % max(cfg.m - rows + 1, 1)
         t0 = time.perf_counter()
         self.orc.msgemm(self.data[r0:r0 + rows], rows, cfg.k, 4, self.vals, self.X, cfg.d,
-                        workers=self.cores)
+                        workers=self.cores if workers is None else workers)
         return time.perf_counter() - t0
 
-    def rows_for(self, target_s):
-        rows = min(self.cfg.m, 256)
-        t = self.run(0, rows)
-        return int(min(self.cfg.m, max(16, rows * target_s / max(t, 1e-4))))
+    def fit(self, workers):
+        """Per-call cost t(rows) = a + c * rows (a: the per-column table builds,
+        c: gathers + row sums), from two sample sizes."""
+        r1, r2 = min(self.cfg.m, 512), min(self.cfg.m, 2048)
+        t1, t2 = self.run(0, r1, workers), self.run(r1, r2, workers)
+        c = max((t2 - t1) / max(r2 - r1, 1), 1e-9)
+        return max(t1 - c * r1, 0.0), c
 
     def gops(self, rows, seconds):
         return 2.0 * rows * self.cfg.k * self.cfg.b / seconds / 1e9
 
-    def describe(self, rows, seconds, nsteps=1):
+    def describe(self, rows, seconds, nsteps=1, workers=None):
         cfg = self.cfg
-        return (f"oracle port (numpy, reference algorithm) on {nsteps} x {rows} rows of "
-                f"{cfg.m} (k={cfg.k}, b={cfg.b}, d={cfg.d}), workers={self.cores}, "
+        what = "the full workload" if rows == cfg.m else f"{rows} rows of {cfg.m}"
+        return (f"oracle port (numpy, reference algorithm) on {nsteps} x {what} "
+                f"(k={cfg.k}, b={cfg.b}, d={cfg.d}), workers={self.cores if workers is None else workers}, "
                 f"{seconds:.2f}s total")
 
 
-def cpu_baseline(cfg, target_s: float = 12.0):
-    """Row chunks of ~1 s each until target_s of CPU work has been timed."""
+def cpu_baseline(cfg, budget_s: float = 30.0):
+    """Both variants of SURVEY.md 8(d): workers=N threads across columns (the
+    reported value: the full workload when it fits the budget) and workers=1
+    as shipped (a row sample, extrapolated to the full workload with the
+    fitted per-call cost)."""
     arm = CpuArm(cfg)
-    rows = arm.rows_for(1.0)
-    total_t, total_rows, n = 0.0, 0, 0
-    while total_t < target_s:
-        total_t += arm.run(total_rows, rows)
-        total_rows += rows
-        n += 1
-    return {"value": arm.gops(total_rows, total_t), "unit": "GOP/s", "cores": arm.cores,
-            "kind": "port", "sample": arm.describe(rows, total_t, n)}
+    variants = []
+    for workers in (arm.cores, 1):
+        a, c = arm.fit(workers)
+        full_est = a + c * cfg.m
+        share = budget_s * (0.6 if workers > 1 else 0.3)
+        rows = cfg.m if full_est <= share else int(min(cfg.m, max(64, (share - a) / c)))
+        t = arm.run(0, rows, workers)
+        v = {"workers": workers, "value": arm.gops(rows, t), "unit": "GOP/s",
+             "sample": arm.describe(rows, t, 1, workers),
+             "full_workload": rows == cfg.m}
+        if rows != cfg.m:
+            v["extrapolated_full_value"] = arm.gops(cfg.m, a + c * cfg.m)
+            v["fit_s"] = {"per_call": a, "per_row": c}
+        variants.append(v)
+    main = variants[0]
+    return {"value": main["value"], "unit": "GOP/s", "cores": arm.cores, "kind": "port",
+            "sample": main["sample"], "same_config": main["full_workload"],
+            "host_cores": arm.host_cores, "variants": variants}
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference's CPU algorithm (oracle port) on this host,
-    each step a bounded row sample; the whole run stays within a few minutes."""
+    """--impl reference: the reference's CPU algorithm (oracle port) on this host
+    with all the threads it can use, each step a bounded row sample (the whole
+    run stays within a few minutes).  The per-call cost fit extrapolates the
+    sample to the full workload (reported beside the measured value)."""
     if rank != 0:
         return
     cfg = CONFIGS[args.config]
     arm = CpuArm(cfg)
+    a, c = arm.fit(arm.cores)
     per_step = min(5.0, max(0.05, 120.0 / max(args.steps + args.warmup, 1)))
-    rows = arm.rows_for(per_step)
+    rows = cfg.m if a + c * cfg.m <= per_step else int(min(cfg.m, max(16, (per_step - a) / c)))
     for i in range(args.warmup):
         arm.run(i * rows, rows)
     total = 0.0
@@ -179,11 +200,15 @@ def run_reference(args, rank, world):
         "scaling": "strong", "vs_baseline": None, "dtype": "f16" if cfg.x_dtype == "float16"
         else cfg.x_dtype, "data": "synthetic (seeded numpy default_rng)", "impl": "reference",
         "config": {"workload": cfg.name, "m": cfg.m, "k": cfg.k, "b": cfg.b, "d": cfg.d,
-                   "step": f"{rows}-row sample of the workload"},
+                   "step": "the full workload" if rows == cfg.m else
+                           f"{rows}-row sample of the workload"},
         "cpu_baseline": {"value": value, "unit": "GOP/s", "cores": arm.cores, "kind": "port",
                          "sample": arm.describe(rows, total, args.steps)},
         "e2e": {"value": value, "unit": "GOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if rows != cfg.m:
+        out["cpu_baseline"].update(extrapolated_full_value=arm.gops(cfg.m, a + c * cfg.m),
+                                   fit_s={"per_call": a, "per_row": c})
     print(json.dumps(out), flush=True)
 
 
@@ -393,6 +418,41 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = tt.item()
 
+    # which LUT kernel the plan runs, and K3 (the one-time weight repack) timed alone
+    plan = next(v for kk, v in pwms[0]._device_cache.items() if kk[0] == "call")
+    kernel_name = {_lib.LAYOUT_LANE: "lane_lut_kernel", _lib.LAYOUT_RB4: "rb_tmem_kernel",
+                   _lib.LAYOUT_RB8: "rb_lut_kernel<4>", _lib.LAYOUT_RB16: "rb_lut_kernel<2>",
+                   _lib.LAYOUT_QUAD: "fused_lut_kernel"}.get(plan.layout, "generic_gemm_kernel")
+    k3 = None
+    if plan.layout != _lib.LAYOUT_NONE:
+        lib = _lib.lib()
+        rep_bytes = int(lib.msg_repacked_bytes(mr, kr, cfg.d, plan.layout))
+        scratch = torch.empty(rep_bytes, dtype=torch.uint8, device=dev)
+        sp = torch.cuda.current_stream().cuda_stream
+
+        def repack(i):
+            _lib.check(lib.msg_repack(_lib.ptr(pwms[i % ncopies].data), mr, kr, cfg.d, plan.layout,
+                                      plan.symmetric, _lib.ptr(scratch), sp))
+        for i in range(2):
+            repack(i)
+        torch.cuda.synchronize()
+        nrep = 6
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(nrep):
+            repack(i)
+        e1.record()
+        torch.cuda.synchronize()
+        ms_k3 = e0.elapsed_time(e1) / nrep
+        k3_bytes = shard_bytes + rep_bytes
+        del scratch
+        k3 = {"kernel": "K3 repack (" + {_lib.LAYOUT_LANE: "lane", _lib.LAYOUT_RB4: "rb4",
+                                           _lib.LAYOUT_RB8: "rb8", _lib.LAYOUT_RB16: "rb16",
+                                           _lib.LAYOUT_QUAD: "quad"}[plan.layout] + " layout)",
+              "ms": ms_k3, "bytes": k3_bytes, "gbs": k3_bytes / (ms_k3 * 1e-3) / 1e9,
+              "frac": k3_bytes / (ms_k3 * 1e-3) / 1e9 / load_peaks()["hbm_gbs"],
+              "note": "one-time per weight matrix, excluded from the step"}
+
     ops = effective_ops(cfg)
     value = ops / (ms_step * 1e-3) / 1e9
     peaks = load_peaks()
@@ -400,7 +460,7 @@ def main():
     x_item = Xh.dtype.itemsize                      # fp16 (or fp32 for config 1)
     f32_tables = exact or x_item == 4
     y_item = 4 if f32_tables else 2
-    lane = cfg.b == 1 and cfg.d == 3 and not f32_tables
+    lane = plan.layout == _lib.LAYOUT_LANE
     bytes_launch = algorithmic_bytes(shard_cfg, x_itemsize=x_item, y_itemsize=y_item)
     achieved = bytes_launch / (ms_lut * 1e-3) / 1e9
     traffic = None
@@ -431,8 +491,7 @@ def main():
                          f">= 3x L2) between steps"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
                      "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-                     "kernel": ("lane_lut_kernel" if lane
-                                else "fused_lut_kernel"), "kernel_ms": ms_lut,
+                     "kernel": kernel_name, "kernel_ms": ms_lut,
                      "kernel_share": ms_lut / ms_step, "algorithmic_bytes_per_launch": bytes_launch,
                      "peak_source": peaks["source"],
                      "smem_lut_bytes_per_launch": smem_bytes,
@@ -448,6 +507,7 @@ def main():
             "ms_per_step": ms_tc, "value": effective_ops(shard_cfg) / (ms_tc * 1e-3) / 1e9,
             "unit": "GOP/s (this rank's shard, no all-gather)",
             "hbm_frac": algorithmic_bytes(shard_cfg, 2, 4) / (ms_tc * 1e-3) / 1e9 / peaks["hbm_gbs"]},
+        "k3_repack": k3,
         "gpu_launches": 2 * args.steps,
         "clocks": clocks,
     }

@@ -227,6 +227,7 @@ class _CallPlan:
                 sub = pwm.row_subset(dev, rows)
                 self.fix = (_CallPlan(sub, dev, stream, b, x_code, x_dtype, d, table_dtype, False,
                                       out_dtype, flags), rows, n_ill)
+        self.layout, self.symmetric = layout.value, sym.value
         x_t = x_dtype if isinstance(x_dtype, t.dtype) else _lib.torch_dtype_of(x_dtype)
         self.x_dtype = x_t
         self.y_dtype = x_t if out_dtype is None else _lib.torch_dtype_of(np.dtype(out_dtype))
