@@ -8,13 +8,16 @@ device is missing, every compute entry point raises.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
 import numpy as np
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "_lib" / "libmsgemm_b200.so"
+# MSG_LIB_VARIANT=debug selects the debug-checks build (tests/test_gpu_debug_build.py)
+LIB_PATH = _PKG / "_lib" / ("libmsgemm_b200_debug.so" if os.environ.get("MSG_LIB_VARIANT") == "debug"
+                            else "libmsgemm_b200.so")
 
 # status codes / enums mirrored from include/msgemm_b200.h
 MSG_OK = 0

@@ -23,6 +23,9 @@ CSRC = PKG / "csrc"
 INCLUDE = ROOT / "include"
 OUTDIR = PKG / "_lib"
 LIB = OUTDIR / "libmsgemm_b200.so"
+# debug variant (device-side bounds asserts + race-provoking barrier jitter,
+# csrc/msg_common.cuh MSG_DEBUG_CHECKS); loaded when MSG_LIB_VARIANT=debug
+LIB_DEBUG = OUTDIR / "libmsgemm_b200_debug.so"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + [
@@ -42,22 +45,26 @@ def sources() -> list[Path]:
     return sorted(CSRC.glob("*.cu"))
 
 
-def _stale() -> bool:
-    if not LIB.exists():
+def _stale(lib: Path = LIB) -> bool:
+    if not lib.exists():
         return True
-    t = LIB.stat().st_mtime
+    t = lib.stat().st_mtime
     deps = list(CSRC.glob("*")) + list(INCLUDE.glob("*.h")) + [Path(__file__)]
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = False) -> Path:
-    if not force and not _stale():
-        return LIB
+def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = False,
+          debug: bool = False) -> Path:
+    lib = LIB_DEBUG if debug else LIB
+    if not force and not _stale(lib):
+        return lib
     OUTDIR.mkdir(exist_ok=True)
-    objdir = OUTDIR / "obj"
+    objdir = OUTDIR / ("obj_debug" if debug else "obj")
     objdir.mkdir(exist_ok=True)
     cc = nvcc()
     extra = ["-Xptxas", "-v"] if ptxas_verbose else []
+    if debug:
+        extra += ["-DMSG_DEBUG_CHECKS=1"]
 
     shared = [p for p in list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h")) + [Path(__file__)]]
     newest_shared = max(p.stat().st_mtime for p in shared)
@@ -79,15 +86,15 @@ def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = Fals
 
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 2)) as ex:
         objs = list(ex.map(compile_one, sources()))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [cc, *ARCH, "-shared", "-o", str(tmp), *map(str, objs)]
     if verbose:
         print(" ".join(cmd), flush=True)
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 def main() -> None:
@@ -95,8 +102,9 @@ def main() -> None:
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-v", "--verbose", action="store_true")
     ap.add_argument("--ptxas", action="store_true", help="print ptxas register/smem usage")
+    ap.add_argument("--debug", action="store_true", help="build the debug-checks variant")
     a = ap.parse_args()
-    print(build(force=a.force or a.ptxas, verbose=a.verbose, ptxas_verbose=a.ptxas))
+    print(build(force=a.force or a.ptxas, verbose=a.verbose, ptxas_verbose=a.ptxas, debug=a.debug))
 
 
 if __name__ == "__main__":

@@ -176,7 +176,38 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// ----------------------------------------------------------------------------
+// debug build (-DMSG_DEBUG_CHECKS, libmsgemm_b200_debug.so; compute-sanitizer
+// is not available on the GPU pool): device-side bounds assertions, and
+// "race provocation" -- a pseudo-random per-warp delay of up to ~2 us in front
+// of every barrier / mbarrier wait / phase switch, so a missing barrier or a
+// read-before-write between warps shows up as a wrong or non-repeatable
+// result in the debug tests.  Both compile to nothing in the release build.
+// ----------------------------------------------------------------------------
+#if defined(MSG_DEBUG_CHECKS)
+#define MSG_DASSERT(cond)                                                              \
+  do {                                                                                 \
+    if (!(cond)) {                                                                     \
+      printf("MSG_DASSERT failed %s:%d block (%d,%d,%d) thread %d: %s\n", __FILE__,   \
+             __LINE__, blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x, #cond);         \
+      __trap();                                                                        \
+    }                                                                                  \
+  } while (0)
+__device__ __forceinline__ void debug_jitter() {
+  uint32_t h = (uint32_t)clock64() * 2654435761u ^ (threadIdx.x >> 5) * 40503u ^ blockIdx.x * 97u;
+  h ^= h >> 13;
+  h *= 0x5bd1e995u;
+  h ^= h >> 15;
+  if ((h & 3) == 0) __nanosleep(h >> 21);   // a quarter of the warps, up to ~2 us
+}
+#define MSG_JITTER() ::msg::debug_jitter()
+#else
+#define MSG_DASSERT(cond) do { } while (0)
+#define MSG_JITTER() do { } while (0)
+#endif
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  MSG_JITTER();
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"

@@ -378,6 +378,7 @@ __global__ void __launch_bounds__(NT, 1) fused_lut_kernel(FusedParams P) {
     mbar_init(&bars[1], 1);
     fence_mbar_init();
   }
+  MSG_JITTER();
   __syncthreads();
   // Launched with PDL: the first weight copy may start before the wait only if
   // the preceding kernel did not write the repacked weights; x is read and the
@@ -419,6 +420,7 @@ __global__ void __launch_bounds__(NT, 1) fused_lut_kernel(FusedParams P) {
     const int64_t g_first = qa * 4;
     const int ngroups = (int)((int64_t)nql * 4 < P.nb - g_first ? (int64_t)nql * 4 : P.nb - g_first);
 
+    MSG_JITTER();
     __syncthreads();  // round t-1 finished with tab, xs0[(t+1)&1] and stage[(t+1)&1]
     if (tid == 0 && t + 1 < nrounds) issue(t + 1);
     float* xs = xs0 + (t & 1) * XN;
@@ -496,6 +498,7 @@ __global__ void __launch_bounds__(NT, 1) fused_lut_kernel(FusedParams P) {
         }
       }
     }
+    MSG_JITTER();
     __syncthreads();
     mbar_wait(&bars[t & 1], (uint32_t)((t >> 1) & 1));
     // ---- gather
@@ -545,8 +548,10 @@ __global__ void __launch_bounds__(NT, 1) fused_lut_kernel(FusedParams P) {
   }
   // ---- fold this slice's symmetry correction beta * sum(x) into every row
   if constexpr (SYM) {
+    MSG_JITTER();
     __syncthreads();
     if (tid < BC) xs0[tid] = P.beta * corr;
+    MSG_JITTER();
     __syncthreads();
     float cv[BC];
 #pragma unroll
@@ -639,11 +644,13 @@ __global__ void __launch_bounds__(256) fused_finish_kernel(
     }
     if constexpr (SG > 1) {
       red[sg][og] = s;
+      MSG_JITTER();
       __syncthreads();
       if (sg == 0) {
 #pragma unroll
         for (int g = 1; g < SG; ++g) s += red[g][og];
       }
+      MSG_JITTER();
       __syncthreads();
     }
     if (t < total && sg == 0) {
@@ -694,6 +701,7 @@ __global__ void __launch_bounds__(256) finish_vec4_kernel(
     }
     if constexpr (SG > 1) {
       red[sg][og] = a;
+      MSG_JITTER();
       __syncthreads();
       if (sg == 0) {
 #pragma unroll
@@ -702,6 +710,7 @@ __global__ void __launch_bounds__(256) finish_vec4_kernel(
           a.x += r.x; a.y += r.y; a.z += r.z; a.w += r.w;
         }
       }
+      MSG_JITTER();
       __syncthreads();
     }
     if (sg != 0 || v >= total4) continue;

@@ -179,6 +179,7 @@ __device__ __forceinline__ void lookup(const uint32_t (&w)[12], uint32_t xt, uin
   uint32_t addr;
   asm("lop3.b32 %0, %1, 0x1FF80, %2, 0xEA;" : "=r"(addr) : "r"(d), "r"(xt));
   asm("lop3.b32 %0, %1, 2, %0, 0xEA;" : "+r"(addr) : "r"(hb));
+  MSG_DASSERT(addr < 128u * 1024u);
   // gather one fp16 entry and accumulate +-entry into fp32; the multiplier is
   // the low (even T) or high (odd T) half of S
   if constexpr (T & 1)
@@ -338,6 +339,7 @@ __global__ void __launch_bounds__(kLaneThreads, 1) lane_lut_kernel(LaneParams P)
       const int nv = min(TPW, ge - gi);
       if (lane == 0) {
         const int slot = issued % kSlots;
+        MSG_DASSERT(nv >= 1 && nv <= TPW && gi + nv <= G1);
         mbar_expect_tx(&bars[slot], nv * kTileBytes);
         bulk_g2s(ring + slot * (TPW * kTileBytes), P.body + (int64_t)gi * kTileBytes,
                  nv * kTileBytes, &bars[slot]);
@@ -382,6 +384,7 @@ __global__ void __launch_bounds__(kLaneThreads, 1) lane_lut_kernel(LaneParams P)
     // ---- build chunk c's 32 bank-private half tables (groups beyond nb get
     // x = 0, i.e. all-zero tables, so padded positions contribute nothing)
     asm volatile("cp.async.wait_group 1;" ::: "memory");  // chunk c landed (c+1 may be in flight)
+    MSG_JITTER();
     __syncthreads();
     const __half* xc = xbuf + (c & 1) * 96 + 3 * lane;
     const float x0 = __half2float(xc[0]), x1 = __half2float(xc[1]), x2 = __half2float(xc[2]);
@@ -413,6 +416,7 @@ __global__ void __launch_bounds__(kLaneThreads, 1) lane_lut_kernel(LaneParams P)
         for (int u0 = 0; u0 < 16; ++u0) dst[u0 * 32] = __hadd2(a2[u0], bc);
       }
     }
+    MSG_JITTER();
     __syncthreads();
     const float corr = *corr_s;
     stage_x(c + 2);  // xbuf[c & 1] is free again: chunk c + 2 goes there

@@ -223,6 +223,7 @@ __global__ void __launch_bounds__(256, 1) dq_mma_kernel(MmaParams P) {
     fence_mbar_init();
   }
   tc_fence_before();
+  MSG_JITTER();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
@@ -330,6 +331,7 @@ __global__ void __launch_bounds__(256, 1) dq_mma_kernel(MmaParams P) {
     }
   }
   tc_fence_before();
+  MSG_JITTER();
   __syncthreads();
   if (warp == 2)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols));

@@ -93,6 +93,7 @@ __global__ void __launch_bounds__(256) repack_rb_kernel(const uint8_t* __restric
   for (int64_t tt = blockIdx.x; tt < ntr * ntq; tt += gridDim.x) {
     const int64_t i0 = (tt % ntr) * kRpTileRows, q0 = (tt / ntr) * kRpTileQuads;
     const int64_t b0 = q0 * 6;  // first byte of the tile in a row
+    MSG_JITTER();
     __syncthreads();
     if ((rb & 3) == 0) {  // 4-byte loads (b0 is a multiple of 4: q0 is a multiple of 16)
       for (int e = threadIdx.x; e < kRpTileRows * 24; e += 256) {
@@ -109,6 +110,7 @@ __global__ void __launch_bounds__(256) repack_rb_kernel(const uint8_t* __restric
         tile[r][c] = (i < m && by < rb) ? packed[i * rb + by] : 0;
       }
     }
+    MSG_JITTER();
     __syncthreads();
     for (int e = threadIdx.x; e < kRpTileRows * kRpTileQuads; e += 256) {
       const int r = e % kRpTileRows, qq = e / kRpTileRows;
@@ -418,10 +420,15 @@ __device__ __forceinline__ void quad_lookups(uint32_t lo, uint32_t hi, uint32_t 
   const uint32_t hm = hi & 0xF000u;
   const uint32_t m02 = lop3_and_or(hm * 0x20008u, 0x80008000u, 0x3C003C00u);
   const uint32_t m13 = lop3_and_or(hm * 0x10004u, 0x80008000u, 0x3C003C00u);
-  gather<BC, 0>(lop3_and_or(lo << 6, 0x1FFC0u, slot[0]) + tab, m02, acc);
-  gather<BC, 0>(lop3_and_or(lo >> 5, 0x1FFC0u, slot[1]) + tab, m13, acc);
-  gather<BC, 1>(lop3_and_or(funnel16(lo, hi), 0x1FFC0u, slot[2]) + tab, m02, acc);
-  gather<BC, 1>(lop3_and_or(hi << 5, 0x1FFC0u, slot[3]) + tab, m13, acc);
+  const uint32_t a0 = lop3_and_or(lo << 6, 0x1FFC0u, slot[0]);
+  const uint32_t a1 = lop3_and_or(lo >> 5, 0x1FFC0u, slot[1]);
+  const uint32_t a2 = lop3_and_or(funnel16(lo, hi), 0x1FFC0u, slot[2]);
+  const uint32_t a3 = lop3_and_or(hi << 5, 0x1FFC0u, slot[3]);
+  MSG_DASSERT(a0 < kRbTableBytes && a1 < kRbTableBytes && a2 < kRbTableBytes && a3 < kRbTableBytes);
+  gather<BC, 0>(a0 + tab, m02, acc);
+  gather<BC, 0>(a1 + tab, m13, acc);
+  gather<BC, 1>(a2 + tab, m02, acc);
+  gather<BC, 1>(a3 + tab, m13, acc);
 }
 
 // One round's weight words of one thread: RPT consecutive rows per quad
@@ -476,10 +483,15 @@ __device__ __forceinline__ void quad_lookups_rot(uint32_t lo, uint32_t hi, uint3
   const uint32_t hm = hi & 0xF000u;
   const uint32_t m02 = lop3_and_or(hm * 0x20008u, 0x80008000u, 0x3C003C00u);
   const uint32_t m13 = lop3_and_or(hm * 0x10004u, 0x80008000u, 0x3C003C00u);
-  gather<BC, 0>(lop3_mux(lo << 6, 0x1FFC0u, t0) + tab, m02, acc);
-  gather<BC, 0>(lop3_mux(lo >> 5, 0x1FFC0u, t0 + 16) + tab, m13, acc);
-  gather<BC, 1>(lop3_mux(funnel16(lo, hi), 0x1FFC0u, t0 + 32) + tab, m02, acc);
-  gather<BC, 1>(lop3_mux(hi << 5, 0x1FFC0u, t0 + 48) + tab, m13, acc);
+  const uint32_t a0 = lop3_mux(lo << 6, 0x1FFC0u, t0);
+  const uint32_t a1 = lop3_mux(lo >> 5, 0x1FFC0u, t0 + 16);
+  const uint32_t a2 = lop3_mux(funnel16(lo, hi), 0x1FFC0u, t0 + 32);
+  const uint32_t a3 = lop3_mux(hi << 5, 0x1FFC0u, t0 + 48);
+  MSG_DASSERT(a0 < kRbTableBytes && a1 < kRbTableBytes && a2 < kRbTableBytes && a3 < kRbTableBytes);
+  gather<BC, 0>(a0 + tab, m02, acc);
+  gather<BC, 0>(a1 + tab, m13, acc);
+  gather<BC, 1>(a2 + tab, m02, acc);
+  gather<BC, 1>(a3 + tab, m13, acc);
 }
 
 template <int BC>
@@ -551,6 +563,7 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_lut_kernel(RbParams P) {
   // `nxt`, gather with `cur` (two register sets, so no copies between rounds)
   auto round = [&](int t, WSet<QR, RPT>& cur, WSet<QR, RPT>& nxt) {
     const __half* xs = xs0 + (t & 1) * kRbXN;
+    MSG_JITTER();
     __syncthreads();  // the gathers of round t-1 are done with the tables; xs[t&1] written
     if (t + 1 < nr && tid < kRbXN) xs0[((t + 1) & 1) * kRbXN + tid] = xnext;
     xnext = load_x(t + 2);
@@ -585,12 +598,14 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_lut_kernel(RbParams P) {
             wv[c] = *reinterpret_cast<const uint32_t*>(&e2);
           }
           uint8_t* p = dst + h * 256 * 64;
+          MSG_DASSERT(p + EB <= smem + kRbTableBytes);
           if constexpr (BC == 2) *reinterpret_cast<uint32_t*>(p) = wv[0];
           else if constexpr (BC == 4) *reinterpret_cast<uint2*>(p) = make_uint2(wv[0], wv[1]);
           else *reinterpret_cast<uint4*>(p) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
         }
       }
     }
+    MSG_JITTER();
     __syncthreads();
     // the next round's words are loaded into the registers of this round's
     // words right after their last use (one register set, no copies): the
@@ -631,6 +646,7 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_lut_kernel(RbParams P) {
   for (int t = 0; t < nr; ++t) round(t, wa, wa);
   // ---- fold this slice's symmetry correction beta * sum(x) into every row
   if (tid < BC) cs[tid] = P.beta * corr;
+  MSG_JITTER();
   __syncthreads();
   float cv[BC];
 #pragma unroll
@@ -773,6 +789,7 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_tmem_kernel(RbParams P) {
   __half xnext = load_x(1);
 
   tm_fence_before();
+  MSG_JITTER();
   __syncthreads();
   tm_fence_after();
   const uint32_t tbase = *tmem_slot + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(warp >> 2) * 128;
@@ -789,6 +806,7 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_tmem_kernel(RbParams P) {
 
   for (int t = 0; t < nr; ++t) {
     const __half* xs = xs0 + (t & 1) * kRbXN;
+    MSG_JITTER();
     __syncthreads();  // the gathers of round t-1 are done with the tables; xs[t&1] written
     if (t + 1 < nr && tid < kRbXN) xs0[((t + 1) & 1) * kRbXN + tid] = xnext;
     xnext = load_x(t + 2);
@@ -819,10 +837,12 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_tmem_kernel(RbParams P) {
             const __half2 e2 = __hfma2(s2, t2[c], b2[c]);
             wv[c] = *reinterpret_cast<const uint32_t*>(&e2);
           }
+          MSG_DASSERT(dst + h * 256 * 64 + 16 <= smem + kRbTableBytes);
           *reinterpret_cast<uint4*>(dst + h * 256 * 64) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
         }
       }
     }
+    MSG_JITTER();
     __syncthreads();
     // ---- gather: row pairs through registers; the next round's words are
     // loaded into the same registers right after their last use
@@ -862,6 +882,7 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_tmem_kernel(RbParams P) {
   // ---- partials: accumulators + this slice's symmetry correction
   if (tid < BC) cs[tid] = P.beta * corr;
   tm_wait_st();
+  MSG_JITTER();
   __syncthreads();
   float cv[BC];
 #pragma unroll
@@ -889,6 +910,7 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_tmem_kernel(RbParams P) {
     }
   }
   tm_fence_before();
+  MSG_JITTER();
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(*tmem_slot));
