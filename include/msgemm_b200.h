@@ -89,6 +89,12 @@ MSG_API const char* msg_last_error(void);
 MSG_API int msg_version(void);
 MSG_API int msg_device_sm_count(void);
 
+/* ---------- host path helpers (no reference counterpart) ---------- */
+/* Launch an instantiated CUDA graph (the drop-in host path's captured
+ * H2D -> msg_gemm -> D2H sequence) on `stream`; sync != 0 also waits for it. */
+MSG_API int msg_graph_run(void* graph_exec, void* stream, int sync);
+MSG_API int msg_stream_sync(void* stream);
+
 /* ---------- packing (packing.py) ---------- */
 
 /* codes (m,k) uint8 -> packed (m,row_bytes) ; packing.py:99-114 _pack_code_rows */

@@ -38,7 +38,7 @@ EXPORTS = (
     "msg_repacked_bytes", "msg_repack", "msg_gemm_plan", "msg_gemm",
     "msg_dequant_mma_workspace_bytes", "msg_dequant_mma",
     "msg_mma_layout_bytes", "msg_repack_mma", "msg_row_conditioning", "msg_copy_rows",
-    "msg_naive_gemm",
+    "msg_naive_gemm", "msg_graph_run", "msg_stream_sync",
 )
 
 _c_i64 = ctypes.c_int64
@@ -70,6 +70,8 @@ _SIGS = {
     "msg_copy_rows": (_c_int, [_vp, _vp, _c_i64, _c_i64, _vp, _c_int, _vp]),
     "msg_naive_gemm": (_c_int, [_vp, _c_int, _vp, _c_int, _c_i64, _c_i64, _c_i64, _c_int, _vp,
                                 _vp]),
+    "msg_graph_run": (_c_int, [_vp, _vp, _c_int]),
+    "msg_stream_sync": (_c_int, [_vp]),
 }
 
 _lib = None
@@ -123,12 +125,20 @@ def check(status: int) -> None:
 # torch / device plumbing
 # --------------------------------------------------------------------------
 
+_torch = None
+_Tensor = None
+
+
 def torch():
-    import torch as _t
-    return _t
+    global _torch
+    if _torch is None:
+        import torch as _t
+        _torch = _t
+    return _torch
 
 
 _dev_ok = False
+_devs = {}
 
 
 def require_device():
@@ -141,7 +151,11 @@ def require_device():
                                "there is no CPU fallback")
         lib()
         _dev_ok = True
-    return t.device("cuda", t.cuda.current_device())
+    i = t.cuda.current_device()
+    d = _devs.get(i)
+    if d is None:
+        d = _devs[i] = t.device("cuda", i)
+    return d
 
 
 def current_stream_handle(dev) -> int:
@@ -184,15 +198,20 @@ _NP2CODE = {
 }
 
 
+_T2CODE = None
+
+
 def dtype_code(dt) -> int:
     """MSG_* element code of a numpy or torch dtype."""
+    global _T2CODE
     t = torch()
     if isinstance(dt, t.dtype):
-        m = {t.float32: F32, t.float16: F16, t.float64: F64, t.int32: I32, t.int64: I64,
-             t.uint8: U8, t.int8: I8, t.int16: I16, t.bfloat16: BF16}
-        if dt not in m:
+        if _T2CODE is None:
+            _T2CODE = {t.float32: F32, t.float16: F16, t.float64: F64, t.int32: I32, t.int64: I64,
+                       t.uint8: U8, t.int8: I8, t.int16: I16, t.bfloat16: BF16}
+        if dt not in _T2CODE:
             raise NotImplementedError(f"dtype {dt} is not supported on the GPU path")
-        return m[dt]
+        return _T2CODE[dt]
     nd = np.dtype(dt)
     if nd not in _NP2CODE:
         raise NotImplementedError(f"dtype {nd} is not supported on the GPU path")
@@ -208,10 +227,13 @@ def torch_dtype_of(np_dtype):
 
 
 def is_torch(x) -> bool:
-    try:
-        return isinstance(x, torch().Tensor)
-    except Exception:  # pragma: no cover
-        return False
+    global _Tensor
+    if _Tensor is None:
+        try:
+            _Tensor = torch().Tensor
+        except Exception:  # pragma: no cover
+            return False
+    return isinstance(x, _Tensor)
 
 
 def to_device(x, dev, non_blocking: bool = False):

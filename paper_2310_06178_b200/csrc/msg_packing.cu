@@ -232,6 +232,17 @@ int msg_version(void) { return 100; }
 
 int msg_device_sm_count(void) { return sm_count(); }
 
+int msg_graph_run(void* graph_exec, void* stream, int sync) {
+  MSG_CUDA_CHECK(cudaGraphLaunch(reinterpret_cast<cudaGraphExec_t>(graph_exec), as_stream(stream)));
+  if (sync) MSG_CUDA_CHECK(cudaStreamSynchronize(as_stream(stream)));
+  return MSG_OK;
+}
+
+int msg_stream_sync(void* stream) {
+  MSG_CUDA_CHECK(cudaStreamSynchronize(as_stream(stream)));
+  return MSG_OK;
+}
+
 int msg_pack_codes(const uint8_t* codes, int64_t m, int64_t k, int width, uint8_t* packed,
                    void* stream) {
   if (int e = check_width(width)) return e;

@@ -1,0 +1,65 @@
+"""The drop-in host path (host X in, host Y out): after the first call with
+given host buffers the H2D copy, the msGeMM kernels and the D2H copy replay
+as one CUDA graph.  Every variant must return the device path's bits, pick
+up new activation values on every call, and keep working across buffers,
+dtypes, vector inputs and the sparse-row fix-up launches."""
+
+import numpy as np
+import pytest
+
+import paper_2310_06178_b200 as mg
+from oracle import msgemm_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def _device_ref(pwm, X, d, **kw):
+    import torch
+    return mg.msgemm(pwm, torch.from_numpy(np.ascontiguousarray(X)).cuda(), d, **kw).cpu().numpy()
+
+
+@pytest.mark.parametrize("m,k,b,dt,kw", [
+    (4096, 4096, 1, np.float16, {}),                      # lane kernel
+    (700, 999, 8, np.float16, {}),                        # rb_tmem
+    (300, 200, 4, np.float16, {}),                        # rb_lut<4>
+    (128, 300, 3, np.float32, {}),                        # fused quad
+    (64, 96, 2, np.float16, {"table_dtype": np.float32, "out_dtype": np.float32}),
+])
+def test_host_calls_replay_the_device_bits(m, k, b, dt, kw):
+    import torch
+    rng = np.random.default_rng(m + k + b)
+    codes = rng.integers(0, 16, (m, k), dtype=np.uint8)
+    codes[7::13] = 0                                      # zero rows: fix-up launches captured too
+    pwm = mg.from_codes(codes, mg.int4_codebook())
+    W = orc.dense(np.asarray(pwm.data), k, 4, orc.int4_values())
+    xpin = torch.empty((k, b), dtype=torch.from_numpy(np.zeros(1, dt)).dtype).pin_memory()
+    y_dt = np.float32 if "out_dtype" in kw else dt
+    ypin = torch.empty((m, b), dtype=torch.from_numpy(np.zeros(1, y_dt)).dtype).pin_memory()
+    ycpu = torch.empty((m, b), dtype=ypin.dtype)
+    for it in range(5):                                  # calls 2.. replay graphs
+        X = rng.standard_normal((k, b)).astype(dt)
+        ref = _device_ref(pwm, X, 3, **kw)
+        assert orc.rel_error(ref.astype(np.float64), W, X) <= (2e-3 if dt == np.float16 else 1e-5)
+        y_np = mg.msgemm(pwm, X, 3, **kw)                                  # numpy in / out
+        assert y_np.dtype == ref.dtype and y_np.tobytes() == ref.tobytes()
+        xpin.copy_(torch.from_numpy(X))
+        y_t = mg.msgemm(pwm, xpin, 3, **kw)                                # pinned in, new tensor out
+        assert y_t.numpy().tobytes() == ref.tobytes()
+        assert mg.msgemm(pwm, xpin, 3, out=ypin, **kw) is ypin              # pinned in and out
+        assert ypin.numpy().tobytes() == ref.tobytes()
+        assert mg.msgemm(pwm, X, 3, out=ycpu, **kw) is ycpu                 # pageable out
+        assert ycpu.numpy().tobytes() == ref.tobytes()
+        if b == 1:
+            yv = mg.msgemm(pwm, X[:, 0], 3, **kw)                          # vector in / out
+            assert yv.shape == (m,) and yv.tobytes() == ref[:, 0].tobytes()
+        assert (y_np[7::13] == 0).all()
+
+
+def test_host_path_results_are_private_copies():
+    rng = np.random.default_rng(1)
+    pwm = mg.from_codes(rng.integers(0, 16, (256, 300), dtype=np.uint8), mg.int4_codebook())
+    X1 = rng.standard_normal((300, 8)).astype(np.float16)
+    X2 = rng.standard_normal((300, 8)).astype(np.float16)
+    ys = [mg.msgemm(pwm, X, 3) for X in (X1, X2, X1, X2, X1)]
+    assert ys[0].tobytes() == ys[2].tobytes() == ys[4].tobytes()
+    assert ys[1].tobytes() == ys[3].tobytes() != ys[0].tobytes()
