@@ -98,45 +98,67 @@ __device__ __forceinline__ uint32_t nib(const uint8_t* row, int64_t j) {
   return (row[j >> 1] >> ((j & 1) * 4)) & 0xF;
 }
 
-// one thread per (quad, padded row): rows fastest so plane stores coalesce
-__global__ void repack_quad_kernel(const uint8_t* __restrict__ packed, int64_t m, int64_t k,
-                                   int d, int rb, int symmetric, QuadLayout L,
-                                   uint8_t* __restrict__ out) {
-  const int64_t total = L.nq * L.mp;
-  const int bits = 4 * d;
+// One CTA per (32 rows, 16 quads): the tile's packed bytes (2d per quad and
+// row) are staged with coalesced loads, then each thread forms (row, quad)
+// records and writes them to the [quad][row] planes (consecutive rows ->
+// coalesced stores).  Position g of row i holds group (g + i) % 4 of the quad
+// (a warp's lanes hit 4 different tables at every step).
+constexpr int kQrRows = 32, kQrQuads = 16;
+__global__ void __launch_bounds__(256) repack_quad_kernel(const uint8_t* __restrict__ packed,
+                                                          int64_t m, int64_t k, int d, int rb,
+                                                          int symmetric, QuadLayout L,
+                                                          uint8_t* __restrict__ out) {
+  __shared__ uint8_t tile[kQrRows][kQrQuads * 6 + 4];
+  const int bits = 4 * d, qb = 2 * d;  // bits per group, bytes per quad
   const uint32_t emask = (1u << bits) - 1;
   const uint32_t top = 1u << (bits - 1);
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t q = t / L.mp, i = t - q * L.mp;
-    uint32_t lo = 0, hi = 0;
-    if (i < m) {
-      const uint8_t* row = packed + i * rb;
-      for (int g = 0; g < 4; ++g) {
-        // position g of row i holds group (g + i) % 4 of the quad (a warp's
-        // lanes hit 4 different tables at every step)
-        const int gi = (int)((g + i) & 3);
-        int64_t j = q * 4 + gi;
-        uint32_t st = 0;
-        if (j < L.nb) {
-          uint32_t idx = 0;
-          for (int r = 0; r < d; ++r) idx |= nib(row, j * d + r) << (4 * r);
-          if (symmetric && (idx & top)) idx = (idx ^ emask) | top;  // complement + sign bit
-          st = idx;
-        }
-        if (d == 1) lo |= st << (4 * g);
-        else if (d == 2) lo |= st << (8 * g);
-        else { lo |= (st & 0xFF) << (8 * g); hi |= (st >> 8) << (4 * g); }
-      }
-      if (L.tail && q == 0) {
-        uint32_t tc = 0;
-        for (int64_t j = L.nb * d; j < k; ++j) tc |= nib(row, j) << (4 * (j - L.nb * d));
-        reinterpret_cast<uint16_t*>(out + L.tail_off)[i] = (uint16_t)tc;
-      }
+  const int64_t ntr = (L.mp + kQrRows - 1) / kQrRows, ntq = (L.nq + kQrQuads - 1) / kQrQuads;
+  for (int64_t tt = blockIdx.x; tt < ntr * ntq; tt += gridDim.x) {
+    const int64_t i0 = (tt % ntr) * kQrRows, q0 = (tt / ntr) * kQrQuads;
+    const int64_t b0 = q0 * qb;
+    const int tb = kQrQuads * qb;  // bytes per tile row
+    __syncthreads();
+    for (int e = threadIdx.x; e < kQrRows * tb; e += 256) {
+      const int r = e / tb, c = e % tb;
+      const int64_t i = i0 + r, by = b0 + c;
+      tile[r][c] = (i < m && by < rb) ? __ldg(packed + i * rb + by) : 0;
     }
-    if (d == 1) reinterpret_cast<uint16_t*>(out + L.lo_off)[t] = (uint16_t)lo;
-    else reinterpret_cast<uint32_t*>(out + L.lo_off)[t] = lo;
-    if (L.has_hi) reinterpret_cast<uint16_t*>(out + L.hi_off)[t] = (uint16_t)hi;
+    __syncthreads();
+    for (int e = threadIdx.x; e < kQrRows * kQrQuads; e += 256) {
+      const int r = e % kQrRows, qq = e / kQrRows;
+      const int64_t i = i0 + r, q = q0 + qq;
+      if (i >= L.mp || q >= L.nq) continue;
+      uint32_t lo = 0, hi = 0;
+      if (i < m) {
+        for (int g = 0; g < 4; ++g) {
+          const int gi = (int)((g + i) & 3);
+          const int64_t j = q * 4 + gi;
+          uint32_t st = 0;
+          if (j < L.nb) {
+            uint32_t idx = 0;
+            for (int r2 = 0; r2 < d; ++r2) {
+              const int cd = qq * 4 * d + gi * d + r2;  // code inside the tile row
+              idx |= ((tile[r][cd >> 1] >> ((cd & 1) * 4)) & 0xF) << (4 * r2);
+            }
+            if (symmetric && (idx & top)) idx = (idx ^ emask) | top;  // complement + sign bit
+            st = idx;
+          }
+          if (d == 1) lo |= st << (4 * g);
+          else if (d == 2) lo |= st << (8 * g);
+          else { lo |= (st & 0xFF) << (8 * g); hi |= (st >> 8) << (4 * g); }
+        }
+        if (L.tail && q == 0) {
+          const uint8_t* row = packed + i * rb;
+          uint32_t tc = 0;
+          for (int64_t j = L.nb * d; j < k; ++j) tc |= nib(row, j) << (4 * (j - L.nb * d));
+          reinterpret_cast<uint16_t*>(out + L.tail_off)[i] = (uint16_t)tc;
+        }
+      }
+      const int64_t t = q * L.mp + i;
+      if (d == 1) reinterpret_cast<uint16_t*>(out + L.lo_off)[t] = (uint16_t)lo;
+      else reinterpret_cast<uint32_t*>(out + L.lo_off)[t] = lo;
+      if (L.has_hi) reinterpret_cast<uint16_t*>(out + L.hi_off)[t] = (uint16_t)hi;
+    }
   }
 }
 
@@ -944,7 +966,8 @@ int msg_repack(const uint8_t* packed, int64_t m, int64_t k, int d, int layout, i
   QuadLayout L = quad_layout(m, k, d);
   int64_t total = L.nq * L.mp;
   if (total == 0) return fail(MSG_ERR_UNSUPPORTED, "quad layout needs at least one full group");
-  int grid = (int)std::min<int64_t>(ceil_div(total, 256), (int64_t)sm_count() * 16);
+  const int64_t tiles = ceil_div(L.mp, kQrRows) * ceil_div(L.nq, kQrQuads);
+  int grid = (int)std::min<int64_t>(tiles, (int64_t)sm_count() * 8);
   repack_quad_kernel<<<grid, 256, 0, as_stream(stream)>>>(packed, m, k, d, row_bytes(k, 4),
                                                          symmetric, L, out);
   MSG_LAUNCH_CHECK();

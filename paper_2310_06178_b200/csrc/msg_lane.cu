@@ -60,31 +60,57 @@ static LaneLayout lane_layout(int64_t m, int64_t k) {
 int64_t lane_layout_bytes(int64_t m, int64_t k) { return lane_layout(m, k).total; }
 int64_t lane_tail_offset(int64_t m, int64_t k) { return lane_layout(m, k).tail_off; }
 
-__device__ __forceinline__ uint32_t nib_l(const uint8_t* row, int64_t j) {
-  return (row[j >> 1] >> ((j & 1) * 4)) & 0xF;
-}
 
-// One thread per (chunk, row): 48 bytes = 10 words of 10-bit "row" fields
-// (position t at bit 10t), one word of signs (positions 2q, 2q+1 at bits
-// 15-q, 31-q, so one shift + LOP3 yields two fp16 +-1 multipliers) and one
-// word of half-select bits (position t at bit t).  Position t of row i holds
-// group t ^ (i % 32) of the chunk.  Stored in the coalesced tile order
-// [chunk][tile][v][lane][4 words].
-__global__ void repack_lane_kernel(const uint8_t* __restrict__ packed, int64_t m, int64_t k,
-                                   int rb, LaneLayout L, uint8_t* __restrict__ out) {
-  const int64_t total = L.nchunk * L.ntiles * 32;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = t / (L.ntiles * 32);
-    const int64_t i = t - c * (L.ntiles * 32);  // padded row
+// One CTA per (32-row tile, 8 chunks): the tile's packed bytes (48 per row
+// and chunk) are staged with coalesced loads, then thread (row, chunk) forms
+// its 48 bytes = 10 words of 10-bit "row" fields (position t at bit 10t), one
+// word of signs (positions 2q, 2q+1 at bits 15-q, 31-q, so one shift + LOP3
+// yields two fp16 +-1 multipliers) and one word of half-select bits
+// (position t at bit t).  Position t of row i holds group t ^ (i % 32) of the
+// chunk.  Stored in the coalesced tile order [chunk][tile][v][lane][4 words].
+constexpr int kLrChunks = 8;
+__global__ void __launch_bounds__(256) repack_lane_kernel(const uint8_t* __restrict__ packed,
+                                                          int64_t m, int64_t k, int rb, LaneLayout L,
+                                                          uint8_t* __restrict__ out) {
+  __shared__ uint8_t tile[32][kLrChunks * 48 + 4];
+  const int tid = threadIdx.x;
+  const int64_t nct = (L.nchunk + kLrChunks - 1) / kLrChunks;
+  for (int64_t t = blockIdx.x; t < L.ntiles * nct; t += gridDim.x) {
+    const int64_t tl = t % L.ntiles, c0 = (t / L.ntiles) * kLrChunks;
+    const int64_t i0 = tl * 32, b0 = c0 * 48;
+    __syncthreads();
+    if ((rb & 3) == 0) {  // b0 = 384 (c0 / 8): 4-byte aligned
+      for (int e = tid; e < 32 * kLrChunks * 12; e += 256) {
+        const int r = e / (kLrChunks * 12), w = e % (kLrChunks * 12);
+        const int64_t i = i0 + r, by = b0 + 4 * w;
+        uint32_t v = 0;
+        if (i < m && by < rb) v = __ldg(reinterpret_cast<const uint32_t*>(packed + i * rb + by));
+        *reinterpret_cast<uint32_t*>(&tile[r][4 * w]) = v;
+      }
+    } else {
+      for (int e = tid; e < 32 * kLrChunks * 48; e += 256) {
+        const int r = e / (kLrChunks * 48), cb = e % (kLrChunks * 48);
+        const int64_t i = i0 + r, by = b0 + cb;
+        tile[r][cb] = (i < m && by < rb) ? __ldg(packed + i * rb + by) : 0;
+      }
+    }
+    __syncthreads();
+    const int lane = tid & 31, cc = tid >> 5;
+    const int64_t c = c0 + cc, i = i0 + lane;
+    if (c >= L.nchunk) continue;
     uint32_t w[12] = {0};
     if (i < m) {
-      const uint8_t* row = packed + i * rb;
       for (int p = 0; p < 32; ++p) {
-        const int64_t j = c * 32 + (p ^ (i & 31));
+        const int gl = p ^ lane;                       // group of position p inside the chunk
+        const int64_t j = c * 32 + gl;
         uint32_t f = 0, sign = 0;
         if (j < L.nb) {
-          uint32_t idx = nib_l(row, 3 * j) | (nib_l(row, 3 * j + 1) << 4) | (nib_l(row, 3 * j + 2) << 8);
+          uint32_t idx = 0;
+#pragma unroll
+          for (int c3 = 0; c3 < 3; ++c3) {
+            const int cd = cc * 96 + 3 * gl + c3;      // code inside the tile row
+            idx |= ((tile[lane][cd >> 1] >> ((cd & 1) * 4)) & 0xF) << (4 * c3);
+          }
           if (idx & 0x800) { idx ^= 0xFFF; sign = 1; }  // sign symmetry: complement
           f = idx;                                       // 11 bits
         }
@@ -92,18 +118,18 @@ __global__ void repack_lane_kernel(const uint8_t* __restrict__ packed, int64_t m
         const int bit = 10 * p;
         w[bit >> 5] |= rowf << (bit & 31);
         if ((bit & 31) > 22) w[(bit >> 5) + 1] |= rowf >> (32 - (bit & 31));
-        // signs of positions 2q, 2q+1 at bits 15-q, 31-q; half select of p at bit p
         w[10] |= sign << ((p & 1) ? 31 - (p >> 1) : 15 - (p >> 1));
         w[11] |= half << p;
       }
       if (L.tail && c == 0) {
+        const uint8_t* row = packed + i * rb;
         uint32_t tc = 0;
-        for (int64_t j = L.nb * 3; j < k; ++j) tc |= nib_l(row, j) << (4 * (j - L.nb * 3));
+        for (int64_t jj = L.nb * 3; jj < k; ++jj)
+          tc |= ((row[jj >> 1] >> ((jj & 1) * 4)) & 0xF) << (4 * (jj - L.nb * 3));
         reinterpret_cast<uint16_t*>(out + L.tail_off)[i] = (uint16_t)tc;
       }
     }
-    const int64_t tile = i >> 5, lane = i & 31;
-    uint4* base = reinterpret_cast<uint4*>(out + L.body_off) + (c * L.ntiles + tile) * 96;
+    uint4* base = reinterpret_cast<uint4*>(out + L.body_off) + (c * L.ntiles + tl) * 96;
     base[0 * 32 + lane] = make_uint4(w[0], w[1], w[2], w[3]);
     base[1 * 32 + lane] = make_uint4(w[4], w[5], w[6], w[7]);
     base[2 * 32 + lane] = make_uint4(w[8], w[9], w[10], w[11]);
@@ -488,7 +514,8 @@ int lane_repack(const uint8_t* packed, int64_t m, int64_t k, uint8_t* out, cudaS
   LaneLayout L = lane_layout(m, k);
   const int64_t total = L.nchunk * L.ntiles * 32;
   if (total == 0) return fail(MSG_ERR_UNSUPPORTED, "lane layout needs at least one group");
-  int grid = (int)std::min<int64_t>(ceil_div(total, 256), (int64_t)sm_count() * 16);
+  const int64_t tiles = L.ntiles * ceil_div(L.nchunk, kLrChunks);
+  int grid = (int)std::min<int64_t>(tiles, (int64_t)sm_count() * 8);
   repack_lane_kernel<<<grid, 256, 0, s>>>(packed, m, k, row_bytes(k, 4), L, out);
   MSG_LAUNCH_CHECK();
   return MSG_OK;

@@ -188,44 +188,50 @@ __constant__ uint8_t kPerms[24] = {0xe4, 0xb4, 0xd8, 0x78, 0x9c, 0x6c, 0xe1, 0xb
 
 __device__ __forceinline__ uint32_t rotr4(uint32_t m, int r) { return ((m >> r) | (m << (4 - r))) & 0xF; }
 
+constexpr int kRb4Cands = 4;  // pairings searched (simulated: top-4 matches top-8, 1.55 wavefronts)
+
 // rotations (2 bits per lane) of one octet from the lanes' 4-bit parity masks
-__device__ uint32_t choose_rotations(const uint32_t (&pm)[8]) {
-  int cand[8], cscore[8], nc = 0;
+// pmw (lane u at bits 4u..4u+3).  The kRb4Cands pairings with the fewest
+// equal-parity (pair, table) incidences are searched over the 24 rotation
+// permutations (ties: earlier pairings first); cand/cscore are this thread's
+// slots in shared memory (dynamically indexed, so not in registers).
+__device__ uint32_t choose_rotations(uint32_t pmw, uint8_t* cand, uint8_t* cscore) {
+  int nc = 0;
   for (int p = 0; p < 105; ++p) {
     const uint32_t code = kPairings[p];
     int sc = 0;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const uint32_t a = (code >> (8 * i)) & 0xF, b = (code >> (8 * i + 4)) & 0xF;
-      sc += __popc(~(pm[a] ^ pm[b]) & 0xF);
+      sc += __popc(~((pmw >> (4 * a)) ^ (pmw >> (4 * b))) & 0xF);
     }
-    if (nc < 8 || sc < cscore[nc - 1]) {  // keep the 8 best (stable: earlier pairings first)
-      int pos = nc < 8 ? nc++ : 7;
+    if (nc < kRb4Cands || sc < cscore[nc - 1]) {  // keep the best (stable: earlier first)
+      int pos = nc < kRb4Cands ? nc++ : kRb4Cands - 1;
       while (pos > 0 && cscore[pos - 1] > sc) {
         cand[pos] = cand[pos - 1];
         cscore[pos] = cscore[pos - 1];
         --pos;
       }
-      cand[pos] = p;
-      cscore[pos] = sc;
+      cand[pos] = (uint8_t)p;
+      cscore[pos] = (uint8_t)sc;
     }
   }
   int best = 99;
   uint32_t best_rho = 0;
   for (int c = 0; c < nc; ++c) {
     const uint32_t code = kPairings[cand[c]];
-    uint32_t rm[4][4];
+    uint32_t rm[4];  // the pair's bad-position mask under rotation r at bits 4r..4r+3
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const uint32_t a = (code >> (8 * i)) & 0xF, b = (code >> (8 * i + 4)) & 0xF;
-      const uint32_t bad = ~(pm[a] ^ pm[b]) & 0xF;
-#pragma unroll
-      for (int r = 0; r < 4; ++r) rm[i][r] = rotr4(bad, r);
+      const uint32_t bad = ~((pmw >> (4 * a)) ^ (pmw >> (4 * b))) & 0xF;
+      rm[i] = bad | (rotr4(bad, 1) << 4) | (rotr4(bad, 2) << 8) | (rotr4(bad, 3) << 12);
     }
     for (int q = 0; q < 24; ++q) {
       const uint32_t pr = kPerms[q];
-      const uint32_t u = rm[0][pr & 3] | rm[1][(pr >> 2) & 3] | rm[2][(pr >> 4) & 3] | rm[3][pr >> 6];
-      const int cost = __popc(u);
+      const uint32_t u = (rm[0] >> (4 * (pr & 3))) | (rm[1] >> (4 * ((pr >> 2) & 3))) |
+                         (rm[2] >> (4 * ((pr >> 4) & 3))) | (rm[3] >> (4 * (pr >> 6)));
+      const int cost = __popc(u & 0xF);
       if (cost < best) {
         best = cost;
         uint32_t rho = 0;
@@ -242,61 +248,95 @@ __device__ uint32_t choose_rotations(const uint32_t (&pm)[8]) {
   return best_rho;
 }
 
-// one work item = (quad q, row block, octet j): rows base + 16 u + r, u < 8, r < 16
+// K3 for rounds of 4 groups.  One CTA per (128-row block, 8 quads): the
+// block's packed bytes (48 per row) are staged with coalesced loads, then
+// thread (r, qq) takes row step r of quad qq: the octet of rows
+// base + 16 u + r (u < 8), its rotations, and its 8 (lo, hi) records; the
+// per-(quad, 16-row group) rotation words are assembled from shared memory.
+constexpr int kRb4Rows = 128, kRb4Quads = 8;
 __global__ void __launch_bounds__(128) repack_rb4_kernel(const uint8_t* __restrict__ packed,
                                                          int64_t m, int64_t k, int rb, RbLayout L,
                                                          uint8_t* __restrict__ out) {
-  const int64_t nblk = (L.mp + 8191) / 8192;
-  const int64_t items = L.nqp * nblk * 64;
+  __shared__ uint8_t tile[kRb4Rows][kRb4Quads * 6 + 4];
+  __shared__ uint16_t rho_s[kRb4Quads][16];
+  __shared__ uint8_t cand_s[128][kRb4Cands], csc_s[128][kRb4Cands];
+  const int tid = threadIdx.x;
   uint32_t* lo_p = reinterpret_cast<uint32_t*>(out + L.lo_off);
   uint16_t* hi_p = reinterpret_cast<uint16_t*>(out + L.hi_off);
   uint32_t* rot_p = reinterpret_cast<uint32_t*>(out + L.rot_off);
-  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < items;
-       it += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t q = it / (nblk * 64), rem = it % (nblk * 64);
-    const int64_t base = (rem / 64) * 8192 + (rem % 64) * 128;
-    if (base >= L.mp) continue;
-    uint32_t rw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int r = 0; r < 16; ++r) {
-      uint32_t f[8][4], sg[8][4], pm[8];
-      for (int u = 0; u < 8; ++u) {
-        const int64_t i = base + 16 * u + r;
-        pm[u] = 0;
-        for (int g = 0; g < 4; ++g) {
-          const int64_t j = q * 4 + g;
-          uint32_t idx = 0, sign = 0;
-          if (i < m && j < L.nb) {
-            const uint8_t* row = packed + i * rb;
-            for (int t = 0; t < 3; ++t) {
-              const int64_t c = 3 * j + t;
-              idx |= ((row[c >> 1] >> ((c & 1) * 4)) & 0xF) << (4 * t);
-            }
-            if (idx & 0x800) { idx ^= 0xFFF; sign = 1; }
-          }
-          f[u][g] = idx;
-          sg[u][g] = sign;
-          pm[u] |= (idx & 1) << g;
-        }
+  const int64_t nrb = L.mp / kRb4Rows + (L.mp % kRb4Rows ? 1 : 0);
+  const int64_t nqt = (L.nqp + kRb4Quads - 1) / kRb4Quads;
+  for (int64_t t = blockIdx.x; t < nrb * nqt; t += gridDim.x) {
+    const int64_t base = (t % nrb) * kRb4Rows, q0 = (t / nrb) * kRb4Quads;
+    const int64_t b0 = q0 * 6;  // first byte of the tile in a row
+    __syncthreads();
+    if ((rb & 3) == 0) {  // b0 = 48 (q0 / 8): 4-byte aligned
+      for (int e = tid; e < kRb4Rows * 12; e += 128) {
+        const int r = e / 12, w = e % 12;
+        const int64_t i = base + r, by = b0 + 4 * w;
+        uint32_t v = 0;
+        if (i < m && by < rb) v = __ldg(reinterpret_cast<const uint32_t*>(packed + i * rb + by));
+        *reinterpret_cast<uint32_t*>(&tile[r][4 * w]) = v;
       }
-      const uint32_t rho = choose_rotations(pm);
+    } else {
+      for (int e = tid; e < kRb4Rows * 48; e += 128) {
+        const int r = e / 48, c = e % 48;
+        const int64_t i = base + r, by = b0 + c;
+        tile[r][c] = (i < m && by < rb) ? __ldg(packed + i * rb + by) : 0;
+      }
+    }
+    __syncthreads();
+    const int r = tid & 15, qq = tid >> 4;
+    const int64_t q = q0 + qq;
+    if (q < L.nqp) {
+      // folded index / sign of group g (of quad q) for tile row tr
+      auto rec = [&](int tr, int g, uint32_t& sign) -> uint32_t {
+        const int64_t j = q * 4 + g;
+        sign = 0;
+        if (base + tr >= m || j >= L.nb) return 0;
+        uint32_t idx = 0;
+#pragma unroll
+        for (int c3 = 0; c3 < 3; ++c3) {
+          const int c = 12 * qq + 3 * g + c3;  // code inside the tile row
+          idx |= ((tile[tr][c >> 1] >> ((c & 1) * 4)) & 0xF) << (4 * c3);
+        }
+        if (idx & 0x800) { idx ^= 0xFFF; sign = 1; }
+        return idx;
+      };
+      uint32_t pmw = 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          uint32_t sg;
+          pmw |= (rec(16 * u + r, g, sg) & 1) << (4 * u + g);
+        }
+      const uint32_t rho = choose_rotations(pmw, cand_s[tid], csc_s[tid]);
+      rho_s[qq][r] = (uint16_t)rho;
+#pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int64_t i = base + 16 * u + r;
+        const int tr = 16 * u + r;
+        const int64_t i = base + tr;
         if (i >= L.mp) continue;
         const uint32_t ru = (rho >> (2 * u)) & 3;
         uint32_t ff[4], ss[4];
-        for (int s2 = 0; s2 < 4; ++s2) {
-          ff[s2] = f[u][(s2 + ru) & 3];
-          ss[s2] = sg[u][(s2 + ru) & 3];
-        }
+#pragma unroll
+        for (int s2 = 0; s2 < 4; ++s2) ff[s2] = rec(tr, (s2 + ru) & 3, ss[s2]);
         lo_p[q * L.mp + i] = ff[0] | (ff[1] << 11) | ((ff[2] & 0x3FF) << 22);
         hi_p[q * L.mp + i] = (uint16_t)((ff[2] >> 10) | (ff[3] << 1) | (ss[0] << 12) |
                                         (ss[1] << 13) | (ss[2] << 14) | (ss[3] << 15));
-        rw[u] |= ru << (2 * r);
       }
     }
-    for (int u = 0; u < 8; ++u) {
-      const int64_t i0 = base + 16 * u;
-      if (i0 < L.mp) rot_p[q * (L.mp / 16) + i0 / 16] = rw[u];
+    __syncthreads();
+    if (tid < kRb4Quads * 8) {  // rotation word of (quad qq2, 16-row group u2): 2 bits per row step
+      const int qq2 = tid >> 3, u2 = tid & 7;
+      const int64_t q2 = q0 + qq2, i0 = base + 16 * u2;
+      if (q2 < L.nqp && i0 < L.mp) {
+        uint32_t w = 0;
+#pragma unroll
+        for (int r2 = 0; r2 < 16; ++r2) w |= ((uint32_t)(rho_s[qq2][r2] >> (2 * u2)) & 3) << (2 * r2);
+        rot_p[q2 * (L.mp / 16) + i0 / 16] = w;
+      }
     }
   }
 }
@@ -937,8 +977,8 @@ int rb_repack(const uint8_t* packed, int64_t m, int64_t k, int G, uint8_t* out, 
                         ((L.nqp + kRpTileQuads - 1) / kRpTileQuads);
   const int grid = (int)std::min<int64_t>(tiles, (int64_t)sm_count() * 16);
   if (G == 4) {
-    const int64_t items = L.nqp * ((L.mp + 8191) / 8192) * 64;
-    const int g4 = (int)std::min<int64_t>(ceil_div(items, 128), (int64_t)sm_count() * 32);
+    const int64_t t4 = ceil_div(L.mp, kRb4Rows) * ceil_div(L.nqp, kRb4Quads);
+    const int g4 = (int)std::min<int64_t>(t4, (int64_t)sm_count() * 16);
     repack_rb4_kernel<<<g4, 128, 0, s>>>(packed, m, k, rb, L, out);
   } else {
     repack_rb_kernel<<<grid, 256, 0, s>>>(packed, m, k, rb, L, out);
