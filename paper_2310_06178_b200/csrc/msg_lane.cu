@@ -322,7 +322,11 @@ __global__ void __launch_bounds__(kLaneThreads, 1) lane_lut_kernel(LaneParams P)
     b = sb + (n * warp) / kNW;
     e = sb + (n * (warp + 1)) / kNW;
   };
-  uint32_t issued = 0, consumed = 0;  // per-warp ring counters
+  // per-warp ring state: next slot to fill / to consume, the consumer's
+  // mbarrier phase, batches in flight (no divisions: kSlots need not be a
+  // power of two)
+  int islot = 0, cslot = 0, inflight = 0;
+  uint32_t cphase = 0;
   int gi, ge, se = min(G1, (G0 / nt + 1) * nt);
   run_of(G0, se, gi, ge);
   auto next_run = [&]() {  // skip to this warp's run in the following segment(s)
@@ -336,16 +340,17 @@ __global__ void __launch_bounds__(kLaneThreads, 1) lane_lut_kernel(LaneParams P)
   next_run();
   // one bulk copy per batch: the batch's tiles are contiguous in HBM
   auto refill = [&]() {
-    while (issued - consumed < (uint32_t)kSlots && gi < G1) {
+    while (inflight < kSlots && gi < G1) {
       const int nv = min(TPW, ge - gi);
       if (lane == 0) {
-        const int slot = issued % kSlots;
+        const int slot = islot;
         MSG_DASSERT(nv >= 1 && nv <= TPW && gi + nv <= G1);
         mbar_expect_tx(&bars[slot], nv * kTileBytes);
         bulk_g2s(ring + slot * (TPW * kTileBytes), P.body + (int64_t)gi * kTileBytes,
                  nv * kTileBytes, &bars[slot]);
       }
-      ++issued;
+      islot = islot + 1 == kSlots ? 0 : islot + 1;
+      ++inflight;
       gi += nv;
       if (gi == ge) next_run();
     }
@@ -427,9 +432,10 @@ __global__ void __launch_bounds__(kLaneThreads, 1) lane_lut_kernel(LaneParams P)
       const int nv = min(TPW, ce - b0);  // tiles of this batch
       uint32_t w[TPW][16];
       {
-        const int slot = consumed % kSlots;
-        mbar_wait(&bars[slot], (consumed / kSlots) & 1);
-        ++consumed;
+        const int slot = cslot;
+        mbar_wait(&bars[slot], cphase);
+        if (++cslot == kSlots) { cslot = 0; cphase ^= 1; }
+        --inflight;
         const uint4* tb = reinterpret_cast<const uint4*>(ring + slot * (TPW * kTileBytes));
 #pragma unroll
         for (int q = 0; q < TPW; ++q) {
