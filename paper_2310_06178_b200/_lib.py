@@ -16,8 +16,10 @@ import numpy as np
 
 _PKG = Path(__file__).resolve().parent
 # MSG_LIB_VARIANT=debug selects the debug-checks build (tests/test_gpu_debug_build.py)
-LIB_PATH = _PKG / "_lib" / ("libmsgemm_b200_debug.so" if os.environ.get("MSG_LIB_VARIANT") == "debug"
-                            else "libmsgemm_b200.so")
+# (MSG_LIB_PATH: an explicit library file, for experiment builds)
+LIB_PATH = Path(os.environ["MSG_LIB_PATH"]) if os.environ.get("MSG_LIB_PATH") else \
+    _PKG / "_lib" / ("libmsgemm_b200_debug.so" if os.environ.get("MSG_LIB_VARIANT") == "debug"
+                     else "libmsgemm_b200.so")
 
 # status codes / enums mirrored from include/msgemm_b200.h
 MSG_OK = 0

@@ -54,17 +54,19 @@ def _stale(lib: Path = LIB) -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = False,
-          debug: bool = False) -> Path:
-    lib = LIB_DEBUG if debug else LIB
+          debug: bool = False, defines: tuple = (), name: str | None = None) -> Path:
+    """defines/name: an experiment build (-D flags) into _lib/<name>.so."""
+    lib = OUTDIR / f"{name}.so" if name else (LIB_DEBUG if debug else LIB)
     if not force and not _stale(lib):
         return lib
     OUTDIR.mkdir(exist_ok=True)
-    objdir = OUTDIR / ("obj_debug" if debug else "obj")
+    objdir = OUTDIR / (f"obj_{name}" if name else ("obj_debug" if debug else "obj"))
     objdir.mkdir(exist_ok=True)
     cc = nvcc()
     extra = ["-Xptxas", "-v"] if ptxas_verbose else []
     if debug:
         extra += ["-DMSG_DEBUG_CHECKS=1"]
+    extra += [f"-D{d}" for d in defines]
 
     shared = [p for p in list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h")) + [Path(__file__)]]
     newest_shared = max(p.stat().st_mtime for p in shared)

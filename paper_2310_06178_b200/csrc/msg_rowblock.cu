@@ -358,6 +358,8 @@ __global__ void repack_rb_tail_kernel(const uint8_t* __restrict__ packed, int64_
 // ============================================================================
 constexpr int kRbTableBytes = 128 * 1024;
 constexpr int kRbXN = 96;                        // staged activations per round (3 G BC)
+// shared memory after the tables: [2][kRbXN] staged x | 8 corrections | TMEM slot | 16 half2 offsets s
+constexpr int kRbCsOff = kRbTableBytes + 2 * kRbXN * 2, kRbS2Off = kRbCsOff + 64;
 
 struct RbParams {
   const uint32_t* lo;     // [nqp][mp]
@@ -441,6 +443,35 @@ __device__ __forceinline__ void gather(uint32_t a, uint32_t mw, float* acc) {
           "fma.rn.f32.f16 %0, l, m1, %0;\n\tfma.rn.f32.f16 %1, h, m1, %1;\n\t}"
           : "+f"(acc[0]), "+f"(acc[1]) : "r"(w0), "r"(mw));
   }
+}
+
+// beta * (sum of this slice's activations of column c0 + c), c < BC, into
+// cs[c] (the sign-symmetric tables' per-column correction, DESIGN.md "Sign
+// symmetry"): computed once after the last round by all threads, in a fixed
+// order (deterministic), with red[] (kRbThreads floats) as scratch -- instead
+// of a serial per-round sum on one warp, which held that warp back at every
+// round's barrier.
+template <int BC, int G>
+__device__ __forceinline__ void slice_correction(const RbParams& P, int r_begin, int r_end,
+                                                 int64_t c0, float* red, float* cs) {
+  const int tid = threadIdx.x;
+  constexpr int NR = kRbThreads / BC;
+  const int c = tid % BC, lr = tid / BC;
+  const int64_t e0 = (int64_t)r_begin * G * 3;
+  const int64_t e1 = min((int64_t)r_end * G, P.nb) * 3;
+  float sum = 0.f;
+  if (c0 + c < P.b)
+    for (int64_t e = e0 + lr; e < e1; e += NR) sum += __half2float(P.x[e * P.b + c0 + c]);
+  red[tid] = sum;
+  MSG_JITTER();
+  __syncthreads();
+  if (tid < BC) {
+    float t = 0.f;
+    for (int i = 0; i < NR; ++i) t += red[i * BC + tid];
+    cs[tid] = P.beta * t;
+  }
+  MSG_JITTER();
+  __syncthreads();
 }
 
 // (a & b) | (c & ~b): the table slot bits come from c, the entry bits from a
@@ -544,9 +575,14 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_lut_kernel(RbParams P) {
   constexpr int NI = G * 256 / kRbThreads;  // build work items per thread
   extern __shared__ __align__(128) uint8_t smem[];
   __half* xs0 = reinterpret_cast<__half*>(smem + kRbTableBytes);  // [2][96] staged activations
-  float* cs = reinterpret_cast<float*>(smem + kRbTableBytes + 2 * kRbXN * 2);  // [BC] corrections
+  float* cs = reinterpret_cast<float*>(smem + kRbCsOff);  // [BC] corrections
+  uint32_t* s2h = reinterpret_cast<uint32_t*>(smem + kRbS2Off);  // half2 (s[c], s[c])
 
   const int tid = threadIdx.x;
+  if (tid < 16) {
+    const __half2 h2 = __float2half2_rn(P.s[tid]);
+    s2h[tid] = *reinterpret_cast<const uint32_t*>(&h2);
+  }
   const int64_t row0 = (int64_t)blockIdx.x * R;
   const int slice = blockIdx.y;
   const int64_t c0 = (int64_t)blockIdx.z * BC;
@@ -586,7 +622,6 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_lut_kernel(RbParams P) {
   for (int r = 0; r < RPT; ++r)
 #pragma unroll
     for (int c = 0; c < BC; ++c) acc[r][c] = 0.f;
-  float corr = 0.f;  // thread tid < BC: sum of the slice's activations of column tid
 
   // table slot (byte offset) of position p: group (p + tid) mod G
   uint32_t slot[QR][4];
@@ -607,11 +642,6 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_lut_kernel(RbParams P) {
     __syncthreads();  // the gathers of round t-1 are done with the tables; xs[t&1] written
     if (t + 1 < nr && tid < kRbXN) xs0[((t + 1) & 1) * kRbXN + tid] = xnext;
     xnext = load_x(t + 2);
-    if (tid < BC) {
-      float sacc = 0.f;
-      for (int e = 0; e < 3 * G; ++e) sacc += __half2float(xs[e * BC + tid]);
-      corr += sacc;
-    }
     // ---- build, all in fp16x2 (the codebook offsets s are exact in fp16):
     // entry(lw + 256 h) = (s[lw & 15] x0 + s[lw >> 4] x1) + s[h] x2, one
     // rounding per operation as in the reference's table (lut.py:59-72)
@@ -623,14 +653,15 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_lut_kernel(RbParams P) {
 #pragma unroll
       for (int i = 0; i < NI; ++i) {
         const int lw = tid / G + i * (kRbThreads / G);
-        const __half2 sa = __float2half2_rn(P.s[lw & 15]), sb = __float2half2_rn(P.s[lw >> 4]);
+        const __half2 sa = *reinterpret_cast<const __half2*>(&s2h[lw & 15]);
+        const __half2 sb = *reinterpret_cast<const __half2*>(&s2h[lw >> 4]);
         __half2 b2[BC / 2];
 #pragma unroll
         for (int c = 0; c < BC / 2; ++c) b2[c] = __hfma2(sb, x1[c], __hmul2(sa, x0[c]));
         uint8_t* dst = bdst + i * (kRbThreads / G) * 64;
 #pragma unroll
         for (int h = 0; h < 8; ++h) {
-          const __half2 s2 = __float2half2_rn(P.s[h]);
+          const __half2 s2 = *reinterpret_cast<const __half2*>(&s2h[h]);
           uint32_t wv[BC / 2];
 #pragma unroll
           for (int c = 0; c < BC / 2; ++c) {
@@ -685,9 +716,9 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_lut_kernel(RbParams P) {
   };
   for (int t = 0; t < nr; ++t) round(t, wa, wa);
   // ---- fold this slice's symmetry correction beta * sum(x) into every row
-  if (tid < BC) cs[tid] = P.beta * corr;
   MSG_JITTER();
-  __syncthreads();
+  __syncthreads();  // the tables are free: scratch for the correction sum
+  slice_correction<BC, G>(P, r_begin, r_end, c0, reinterpret_cast<float*>(smem), cs);
   float cv[BC];
 #pragma unroll
   for (int c = 0; c < BC; ++c) cv[c] = cs[c];
@@ -767,10 +798,15 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_tmem_kernel(RbParams P) {
   constexpr int BC = 8, G = 4, EB = 16, NI = G * 256 / kRbThreads;
   extern __shared__ __align__(128) uint8_t smem[];
   __half* xs0 = reinterpret_cast<__half*>(smem + kRbTableBytes);                // [2][96]
-  float* cs = reinterpret_cast<float*>(smem + kRbTableBytes + 2 * kRbXN * 2);   // [8]
+  float* cs = reinterpret_cast<float*>(smem + kRbCsOff);   // [8]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cs + 8);
+  uint32_t* s2h = reinterpret_cast<uint32_t*>(smem + kRbS2Off);  // half2 (s[c], s[c])
 
   const int tid = threadIdx.x, warp = tid >> 5;
+  if (tid < 16) {
+    const __half2 h2 = __float2half2_rn(P.s[tid]);
+    s2h[tid] = *reinterpret_cast<const uint32_t*>(&h2);
+  }
   const int64_t row0 = (int64_t)blockIdx.x * kTmR;
   const int slice = blockIdx.y;
   const int64_t c0 = (int64_t)blockIdx.z * BC;
@@ -840,7 +876,6 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_tmem_kernel(RbParams P) {
 #pragma unroll
     for (int p = 0; p < kTmRPT / 2; ++p) tm_st16(tbase + 16 * p, z);
   }
-  float corr = 0.f;
   const int tt = tid % G;
   uint8_t* const bdst = smem + (uint32_t)(tid / G) * 64 + (uint32_t)tt * EB;
 
@@ -850,11 +885,6 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_tmem_kernel(RbParams P) {
     __syncthreads();  // the gathers of round t-1 are done with the tables; xs[t&1] written
     if (t + 1 < nr && tid < kRbXN) xs0[((t + 1) & 1) * kRbXN + tid] = xnext;
     xnext = load_x(t + 2);
-    if (tid < BC) {
-      float sacc = 0.f;
-      for (int e = 0; e < 3 * G; ++e) sacc += __half2float(xs[e * BC + tid]);
-      corr += sacc;
-    }
     {  // ---- build (as rb_lut_kernel)
       const __half2* xg = reinterpret_cast<const __half2*>(xs + tt * 3 * BC);
       __half2 x0[BC / 2], x1[BC / 2], t2[BC / 2];
@@ -863,14 +893,15 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_tmem_kernel(RbParams P) {
 #pragma unroll
       for (int i = 0; i < NI; ++i) {
         const int lw = tid / G + i * (kRbThreads / G);
-        const __half2 sa = __float2half2_rn(P.s[lw & 15]), sb = __float2half2_rn(P.s[lw >> 4]);
+        const __half2 sa = *reinterpret_cast<const __half2*>(&s2h[lw & 15]);
+        const __half2 sb = *reinterpret_cast<const __half2*>(&s2h[lw >> 4]);
         __half2 b2[BC / 2];
 #pragma unroll
         for (int c = 0; c < BC / 2; ++c) b2[c] = __hfma2(sb, x1[c], __hmul2(sa, x0[c]));
         uint8_t* dst = bdst + i * (kRbThreads / G) * 64;
 #pragma unroll
         for (int h = 0; h < 8; ++h) {
-          const __half2 s2 = __float2half2_rn(P.s[h]);
+          const __half2 s2 = *reinterpret_cast<const __half2*>(&s2h[h]);
           uint32_t wv[BC / 2];
 #pragma unroll
           for (int c = 0; c < BC / 2; ++c) {
@@ -920,10 +951,10 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_tmem_kernel(RbParams P) {
     }
   }
   // ---- partials: accumulators + this slice's symmetry correction
-  if (tid < BC) cs[tid] = P.beta * corr;
   tm_wait_st();
   MSG_JITTER();
-  __syncthreads();
+  __syncthreads();  // the tables are free: scratch for the correction sum
+  slice_correction<BC, G>(P, r_begin, r_end, c0, reinterpret_cast<float*>(smem), cs);
   float cv[BC];
 #pragma unroll
   for (int c = 0; c < BC; ++c) cv[c] = cs[c];
@@ -1012,7 +1043,7 @@ RbPlan rb_plan(int64_t m, int64_t k, int64_t b) {
   p.rps = (int)ceil_div(p.nrounds, S);
   p.S = (int)ceil_div(p.nrounds, p.rps);
   p.partial_bytes = al256((int64_t)p.S * m * b * 4);
-  p.smem = kRbTableBytes + 2 * kRbXN * 2 + 64;  // tables, staged x, corrections, TMEM slot
+  p.smem = kRbS2Off + 64;  // tables, staged x, corrections, TMEM slot, s offsets
   return p;
 }
 
