@@ -186,6 +186,15 @@ MSG_API int msg_dequant_mma(const uint8_t* wmma, int64_t m, int64_t k, const dou
                             const void* x, int x_dtype, int64_t b, void* y, int y_dtype,
                             void* workspace, int64_t workspace_bytes, void* stream);
 
+/* Dense comparison baseline for small batches: Y (m,b) = dequant(W) @ X from
+ * the reference packed layout (no repack), int4/uint4 codebooks, fp16 X,
+ * 1 <= b <= 8, rows of a multiple of 16 bytes (k % 32 == 0); CUDA-core
+ * dequantise + exact fp16 x fp16 -> fp32 FMAs, HBM-bound at b = 1..2.
+ * gemm.py:206-216 naive_gemm(dense(pwm), X) semantics as msg_dequant_mma. */
+MSG_API int msg_dequant_gemv(const uint8_t* packed, int64_t m, int64_t k, const double* values,
+                             const void* x, int x_dtype, int64_t b, void* y, int y_dtype,
+                             void* stream);
+
 /* ---------- dense reference product (gemm.py:206-216 naive_gemm) ---------- */
 /* Y (m,b) = W (m,k) @ X (k,b), operands of any supported dtype, converted
  * in-kernel.  mode 0: both integer -> int64 Y, wrapping int64 arithmetic

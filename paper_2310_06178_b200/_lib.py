@@ -40,7 +40,7 @@ EXPORTS = (
     "msg_repacked_bytes", "msg_repack", "msg_gemm_plan", "msg_gemm",
     "msg_dequant_mma_workspace_bytes", "msg_dequant_mma",
     "msg_mma_layout_bytes", "msg_repack_mma", "msg_row_conditioning", "msg_copy_rows",
-    "msg_naive_gemm", "msg_graph_run", "msg_stream_sync",
+    "msg_naive_gemm", "msg_graph_run", "msg_stream_sync", "msg_dequant_gemv",
 )
 
 _c_i64 = ctypes.c_int64
@@ -73,6 +73,7 @@ _SIGS = {
     "msg_naive_gemm": (_c_int, [_vp, _c_int, _vp, _c_int, _c_i64, _c_i64, _c_i64, _c_int, _vp,
                                 _vp]),
     "msg_graph_run": (_c_int, [_vp, _vp, _c_int]),
+    "msg_dequant_gemv": (_c_int, [_vp, _c_i64, _c_i64, _vp, _vp, _c_int, _c_i64, _vp, _c_int, _vp]),
     "msg_stream_sync": (_c_int, [_vp]),
 }
 

@@ -507,12 +507,18 @@ def naive_gemm_counted(W, X):
     return Y, OpCount(fma=m * k * b, mem_weights=m * k, mem_activations=k * b)
 
 
-def dequant_gemm(pwm: PackedWeightMatrix, X, out_dtype=np.float32, out=None):
-    """Dense comparison baseline: dequantise int4 W to fp16 and multiply on the
-    tcgen05 tensor cores (K4, csrc/msg_mma.cu); fp32 accumulation in TMEM.
+_GEMV_MAX_B = 1   # dense baseline: CUDA-core GEMV at b = 1, tcgen05 above (measured: tie at b = 2)
+
+
+def dequant_gemm(pwm: PackedWeightMatrix, X, out_dtype=np.float32, out=None, kernel="auto"):
+    """Dense comparison baseline (K4): dequantise int4 W and multiply, fp32
+    accumulation -- on the CUDA cores straight from the packed layout for
+    small batches (csrc/msg_dense.cu, weight-stream bound), else on the
+    tcgen05 tensor cores (csrc/msg_mma.cu, accumulator in TMEM).
 
     X must be fp16 (k,) or (k, b) with b <= 256; int4/uint4 codebooks, no
     scales.  Same result contract as naive_gemm(dense(pwm), X) (gemm.py:206-216).
+    kernel: "auto" | "gemv" (b <= 8, k % 32 == 0) | "mma".
     """
     pwm = _ensure_device_pwm(pwm)
     if pwm.scales is not None:
@@ -527,7 +533,18 @@ def dequant_gemm(pwm: PackedWeightMatrix, X, out_dtype=np.float32, out=None):
     xd = _lib.to_device(Xm, dev)
     y_dt = _lib.torch_dtype_of(np.dtype(out_dtype))
     Y = out if out is not None else t.empty((m, b), dtype=y_dt, device=dev)
-    if m and b:
+    cbv = [float(v) for v in pwm.codebook.values]
+    nib = cbv == [float(c if c < 8 else c - 16) for c in range(16)] or cbv == [float(c) for c in range(16)]
+    gemv_ok = b <= 8 and k % 32 == 0 and nib and xd.dtype == t.float16
+    use_gemv = gemv_ok and (kernel == "gemv" or (kernel == "auto" and b <= _GEMV_MAX_B))
+    if kernel == "gemv" and not gemv_ok:
+        raise NotImplementedError("the GEMV baseline needs b <= 8, k % 32 == 0, int4/uint4 and fp16 X")
+    if m and b and use_gemv:
+        _lib.check(lib.msg_dequant_gemv(
+            _lib.ptr(pwm.device_data(dev)), m, k, _lib.host_doubles(pwm.codebook.values),
+            _lib.ptr(xd.contiguous()), _lib.dtype_code(xd.dtype), b, _lib.ptr(Y),
+            _lib.dtype_code(y_dt), _lib.stream_ptr()))
+    elif m and b:
         wt = pwm.device_mma_layout(dev)
         ws = _lib.workspace(lib.msg_dequant_mma_workspace_bytes(m, k, b), dev)
         _lib.check(lib.msg_dequant_mma(
