@@ -49,4 +49,4 @@ for (m, k, bs) in ((8192, 8192, (1, 2, 4, 8, 16)), (4096, 4096, (1,)), (65536, 8
             us = e0.elapsed_time(e1) * 1e3 / (5 * n)
             byts = m * k / 2 + k * b * 2 + m * b * 4
             print(f"{m}x{k} b={b:3d} {kern:4s} {us:8.1f} us  {byts / us / 1e3:7.0f} GB/s  "
-                  f"({byts / us / 1e3 / PEAK:.1%} HBM)  {2 * m * k * b / us / 1e6:8.0f} GOP/s", flush=True)
+                  f"({byts / us / 1e3 / PEAK:.1%} HBM)  {2 * m * k * b / us / 1e6:8.1f} TOP/s", flush=True)
