@@ -71,6 +71,7 @@ def _check_scales_for_depth(pwm, d: int) -> None:
 
 
 _T2NP = None
+_HOST_Y_DIRECT = __import__("os").environ.get("MSG_HOST_Y", "direct") != "copy"
 
 
 def _np_dtype(X):
@@ -110,6 +111,16 @@ def msgemm(pwm: PackedWeightMatrix, X, d: int, budget: int = DEFAULT_BUDGET,
         e.g. float32 Y from fp16 X (the bit-exact integer check).
     out: optional preallocated CUDA tensor for Y (torch inputs only).
     """
+    # repeated host-path calls with the same X / out objects (a serving loop
+    # reusing its pinned buffers): validation and plan lookup were done on
+    # the first call; only the buffers' identity, shape and stream are checked
+    fast = getattr(pwm, "_device_cache", None)
+    if fast is not None:
+        ent = fast.get(("fast", id(X), id(out), d, budget, table_dtype, symmetric, out_dtype, _flags))
+        if ent is not None:
+            res = ent(X, out)
+            if res is not None:
+                return res
     pwm = _ensure_device_pwm(pwm)
     is_tensor = _lib.is_torch(X)
     Xm, was_vector = _as_matrix(X, is_tensor)
@@ -155,15 +166,10 @@ def msgemm(pwm: PackedWeightMatrix, X, d: int, budget: int = DEFAULT_BUDGET,
     # host activations and/or host output: the plan's pinned + device staging
     # buffers are shared by calls on this stream, so one call uses them at a time
     if not on_device and dev_out is None and m and b:
-        with call.lock:                # host in, host out: the graph-replayed path
-            Yh = call.run_host(Xm, host_out, stream)
-            if host_out is not None:
-                if Yh is not host_out:
-                    host_out.copy_(Yh.reshape(host_out.shape))
-                return host_out
-            Yh = Yh.clone() if is_tensor else Yh.numpy().copy()
-        Yh = Yh[:, 0] if was_vector else Yh
-        return Yh
+        res = _host_call(call, Xm, host_out, stream, is_tensor, was_vector)
+        _register_fast(pwm, X, out, (d, budget, table_dtype, symmetric, out_dtype, _flags), call,
+                       stream, dev, is_tensor, was_vector)
+        return res
     with call.lock:
         xd = call.device_x(Xm) if on_device else call.stage_x(Xm)
         Y = dev_out if dev_out is not None else call.y_stage()
@@ -177,6 +183,53 @@ def msgemm(pwm: PackedWeightMatrix, X, d: int, budget: int = DEFAULT_BUDGET,
         Yh = call.y_host(Y)           # D2H into pinned staging, then a private copy
     Yh = Yh[:, 0] if was_vector else Yh
     return Yh if is_tensor else Yh.numpy()
+
+
+def _host_call(call, Xm, host_out, stream, is_tensor, was_vector):
+    """Host X in, host Y out through the plan's graph-replayed path."""
+    with call.lock:
+        Yh = call.run_host(Xm, host_out, stream)
+        if host_out is not None:
+            if Yh is not host_out:
+                host_out.copy_(Yh.reshape(host_out.shape))
+            return host_out
+        Yh = Yh.clone() if is_tensor else Yh.numpy().copy()
+    return Yh[:, 0] if was_vector else Yh
+
+
+def _register_fast(pwm, X, out, opts, call, stream, dev, is_tensor, was_vector):
+    """Remember a validated host-path call keyed by the identity of X and out.
+    The entry re-checks that X / out are the same live objects with the same
+    shape, dtype and data pointer and that the current stream is unchanged;
+    anything else falls back to the full path (returns None)."""
+    import weakref
+    try:
+        xref = weakref.ref(X)
+        oref = weakref.ref(out) if out is not None else (lambda: None)
+    except TypeError:           # e.g. a list: not weak-referenceable, no fast path
+        return
+    xshape, xdtype = X.shape, X.dtype
+    xptr = X.data_ptr() if is_tensor else X.ctypes.data
+    oshape = out.shape if out is not None else None
+    optr = out.data_ptr() if out is not None else None
+    key = ("fast", id(X), id(out)) + opts
+
+    def ent(X2, out2):
+        if xref() is not X2 or X2.shape != xshape or X2.dtype != xdtype:
+            return None
+        if (X2.data_ptr() if is_tensor else X2.ctypes.data) != xptr:
+            return None
+        if out2 is not None and (oref() is not out2 or out2.shape != oshape or out2.data_ptr() != optr):
+            return None
+        if _lib.current_stream_handle(dev) != stream or _lib.torch().cuda.current_device() != dev.index:
+            return None
+        return _host_call(call, X2[:, None] if was_vector else X2, out2, stream, is_tensor, was_vector)
+
+    cache = pwm._device_cache
+    if sum(1 for kk in cache if kk[0] == "fast") >= 8:
+        for kk in [kk for kk in cache if kk[0] == "fast"]:
+            del cache[kk]
+    cache[key] = ent
 
 
 # Sign-symmetric half tables (csrc msg_fused.cu / msg_lane.cu) round entries
@@ -330,12 +383,23 @@ class _CallPlan:
             _lib.check(self._graph_run(ex[1], stream, 1))
         else:
             self._seen.add(key)
-            ys = self.y_stage()
             self._xs.copy_(src, non_blocking=True)
-            self.launch(self._xs, ys)
-            dst.copy_(ys.reshape(dst.shape), non_blocking=True)
+            self._launch_to_host(dst)
             _lib.check(_lib.lib().msg_stream_sync(_lib.ctypes.c_void_p(stream)))
         return dst
+
+    def _launch_to_host(self, dst, stream=None):
+        """Kernels -> Y in host memory.  For b >= 2 the finishing kernels store
+        Y straight into the pinned buffer (device-visible under UVA), so no
+        separate D2H copy trails the kernels (cfg5 e2e 272 -> 263 us); the
+        b = 1 finish writes 2-byte values, which measured faster through a
+        device Y + one D2H copy.  MSG_HOST_Y=copy forces the copy (A/B)."""
+        if _HOST_Y_DIRECT and self.b >= 2:
+            self.launch(self._xs, dst.reshape(self.m, self.b), stream)
+        else:
+            ys = self.y_stage()
+            self.launch(self._xs, ys, stream)
+            dst.copy_(ys.reshape(dst.shape), non_blocking=True)
 
     def _xh_np(self):
         if self._xh_view is None or self._xh_view[0] is not self._xh:
@@ -355,8 +419,7 @@ class _CallPlan:
         with t.cuda.stream(side):
             with t.cuda.graph(g, stream=side, capture_error_mode="thread_local"):
                 self._xs.copy_(src, non_blocking=True)
-                self.launch(self._xs, ys, side.cuda_stream)
-                dst.copy_(ys.reshape(dst.shape), non_blocking=True)
+                self._launch_to_host(dst, side.cuda_stream)
         cur.wait_stream(side)
         ex = (g, _lib.ctypes.c_void_p(int(g.raw_cuda_graph_exec())))
         self._graphs[(src.data_ptr(), dst.data_ptr())] = ex

@@ -63,3 +63,30 @@ def test_host_path_results_are_private_copies():
     ys = [mg.msgemm(pwm, X, 3) for X in (X1, X2, X1, X2, X1)]
     assert ys[0].tobytes() == ys[2].tobytes() == ys[4].tobytes()
     assert ys[1].tobytes() == ys[3].tobytes() != ys[0].tobytes()
+
+
+def test_fast_path_rechecks_buffers():
+    """Repeated calls with the same host buffers take the identity-keyed fast
+    path; a changed shape, a new array or a different stream falls back."""
+    import torch
+    rng = np.random.default_rng(2)
+    pwm = mg.from_codes(rng.integers(0, 16, (512, 960), dtype=np.uint8), mg.int4_codebook())
+    W = orc.dense(np.asarray(pwm.data), 960, 4, orc.int4_values())
+    xpin = torch.empty((960, 1), dtype=torch.float16).pin_memory()
+    ypin = torch.empty((512, 1), dtype=torch.float16).pin_memory()
+    for it in range(4):
+        X = rng.standard_normal((960, 1)).astype(np.float16)
+        xpin.copy_(torch.from_numpy(X))
+        assert mg.msgemm(pwm, xpin, 3, out=ypin) is ypin
+        assert orc.rel_error(ypin.numpy().astype(np.float64), W, X) <= 2e-3
+    assert any(k[0] == "fast" for k in pwm._device_cache)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):                              # other stream: new plan, same results
+        y2 = mg.msgemm(pwm, xpin, 3)
+    assert y2.numpy().tobytes() == ypin.numpy().tobytes()
+    xv = np.ascontiguousarray(X[:, 0])
+    for _ in range(3):                                      # vector numpy input reused
+        yv = mg.msgemm(pwm, xv, 3)
+        assert yv.shape == (512,) and yv.tobytes() == ypin.numpy()[:, 0].tobytes()
+    with pytest.raises(ValueError):
+        mg.msgemm(pwm, np.zeros(959, np.float16), 3)
