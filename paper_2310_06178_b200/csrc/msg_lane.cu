@@ -317,10 +317,10 @@ __global__ void __launch_bounds__(kLaneThreads, 1) lane_lut_kernel(LaneParams P)
   // [sb + n w / 16, sb + n (w + 1) / 16), n = se - sb, consumed TPW at a time.
   // Issue cursor (lane-uniform): next tile gi of the run ending at ge, in the
   // segment ending at se; gi == G1 when the CTA's range is exhausted.
-  auto run_of = [&](int sb, int se, int& b, int& e) {
-    const int n = se - sb;
-    b = sb + (n * warp) / kNW;
-    e = sb + (n * (warp + 1)) / kNW;
+  auto run_of = [&](int sb, int se, int& b, int& e) {  // unsigned: shifts, no signed division
+    const uint32_t n = (uint32_t)(se - sb);
+    b = sb + (int)((n * (uint32_t)warp) / kNW);
+    e = sb + (int)((n * (uint32_t)(warp + 1)) / kNW);
   };
   // per-warp ring state: next slot to fill / to consume, the consumer's
   // mbarrier phase, batches in flight (no divisions: kSlots need not be a
@@ -338,7 +338,26 @@ __global__ void __launch_bounds__(kLaneThreads, 1) lane_lut_kernel(LaneParams P)
     }
   };
   next_run();
-  // one bulk copy per batch: the batch's tiles are contiguous in HBM
+  // one bulk copy per batch: the batch's tiles are contiguous in HBM.
+  // refill_one() issues at most one batch (the steady state: one per
+  // consumed batch, which keeps the bookkeeping per tile short); refill()
+  // fills every free slot (the prologue)
+  auto refill_one = [&]() {
+    if (inflight < kSlots && gi < G1) {
+      const int nv = min(TPW, ge - gi);
+      if (lane == 0) {
+        const int slot = islot;
+        MSG_DASSERT(nv >= 1 && nv <= TPW && gi + nv <= G1);
+        mbar_expect_tx(&bars[slot], nv * kTileBytes);
+        bulk_g2s(ring + slot * (TPW * kTileBytes), P.body + (int64_t)gi * kTileBytes,
+                 nv * kTileBytes, &bars[slot]);
+      }
+      islot = islot + 1 == kSlots ? 0 : islot + 1;
+      ++inflight;
+      gi += nv;
+      if (gi == ge) next_run();
+    }
+  };
   auto refill = [&]() {
     while (inflight < kSlots && gi < G1) {
       const int nv = min(TPW, ge - gi);
@@ -452,7 +471,7 @@ __global__ void __launch_bounds__(kLaneThreads, 1) lane_lut_kernel(LaneParams P)
         }
       }
       __syncwarp();  // every lane has copied its words out of the consumed slots
-      refill();
+      refill_one();
       float acc[TPW][2];
 #pragma unroll
       for (int q = 0; q < TPW; ++q) { acc[q][0] = corr; acc[q][1] = 0.f; }
