@@ -242,10 +242,19 @@ def main():
     from paper_2310_06178_b200 import _lib
     from paper_2310_06178_b200.workloads import activations, weights
 
+    # functional test of the N > 1 code path on a one-GPU box only
+    # (tests/test_bench_multirank.py): every rank on cuda:0, gloo collectives.
+    # Never a measurement: ranks sharing a GPU are not N GPUs.
+    share = os.environ.get("MSG_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     cfg = CONFIGS[args.config]
     ksplit = world > 1 and args.split == "k"
     X = activations(cfg)
@@ -284,7 +293,16 @@ def main():
     Yfull = torch.empty((cfg.m, cfg.b), dtype=y_dt, device=dev) if world > 1 else Yshard
 
     def collective():
-        if ksplit:
+        if share:      # gloo functional test: host-staged collectives
+            if ksplit:
+                h = Yshard.cpu()
+                dist.all_reduce(h, op=dist.ReduceOp.SUM)
+                Yshard.copy_(h)
+            else:
+                h = torch.empty((cfg.m, cfg.b), dtype=Yshard.dtype)
+                dist.all_gather_into_tensor(h, Yshard.cpu())
+                Yfull.copy_(h)
+        elif ksplit:
             dist.all_reduce(Yshard, op=dist.ReduceOp.SUM)   # Yshard: this rank's fp32 partial
         else:
             dist.all_gather_into_tensor(Yfull, Yshard)
@@ -353,7 +371,7 @@ def main():
         barrier()
         ms = e0.elapsed_time(e1)
         if world > 1:
-            tt = torch.tensor([ms], device=dev)
+            tt = torch.tensor([ms], device="cpu" if share else dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ms = tt.item()
         return ms / nsteps
@@ -414,7 +432,7 @@ def main():
     barrier()
     e2e_ms = 1e3 * (time.perf_counter() - t0) / e2e_steps
     if world > 1:
-        tt = torch.tensor([e2e_ms], device=dev)
+        tt = torch.tensor([e2e_ms], device="cpu" if share else dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = tt.item()
 
