@@ -23,6 +23,7 @@ import numpy as np
 from . import _lib
 from ._lib import TableBudgetError
 from .lut import DEFAULT_BUDGET, block_nbytes, build_lut
+from .codebook import Codebook
 from .packing import PackedWeightMatrix, PerGroup, PerRow, group_indices
 
 __all__ = ["OpCount", "msgemm", "msgemm_counted", "msgemm_traced", "naive_gemm",
@@ -86,12 +87,39 @@ def _np_dtype(X):
     return X.dtype
 
 
+_FOREIGN = {}   # id(foreign pwm) -> (weakref to it, our wrapper, its scales, its codebook)
+
+
 def _ensure_device_pwm(pwm):
-    """Accept our PackedWeightMatrix or any duck-typed equivalent (e.g. the reference's)."""
+    """Accept our PackedWeightMatrix or any duck-typed equivalent (e.g. the
+    reference's).  A foreign object is wrapped once and the wrapper (with its
+    device copies, layouts and call plans) reused while the object lives and
+    still holds the same arrays, so a reference user's repeated calls do not
+    repack the weights every time."""
     if isinstance(pwm, PackedWeightMatrix):
         return pwm
-    return PackedWeightMatrix(m=pwm.m, k=pwm.k, width=pwm.width, data=pwm.data,
-                              codebook=pwm.codebook, scales=pwm.scales)
+    ent = _FOREIGN.get(id(pwm))
+    if ent is not None:
+        ref, ours = ent[0], ent[1]
+        if ref() is pwm and ours.data is pwm.data and ent[2] is pwm.scales and ent[3] is pwm.codebook:
+            return ours
+    cb = pwm.codebook
+    if not isinstance(cb, Codebook):       # the reference's Codebook: same fields
+        cb = Codebook(width=int(cb.width), values=tuple(cb.values))
+    sc = pwm.scales
+    if sc is not None and not isinstance(sc, (PerRow, PerGroup)):
+        sc = (PerGroup(group_size=int(sc.group_size), q=sc.q) if hasattr(sc, "group_size")
+              else PerRow(q=sc.q))
+    ours = PackedWeightMatrix(m=pwm.m, k=pwm.k, width=pwm.width, data=pwm.data,
+                              codebook=cb, scales=sc)
+    try:
+        import weakref
+        key = id(pwm)
+        ref = weakref.ref(pwm, lambda _r, key=key: _FOREIGN.pop(key, None))
+        _FOREIGN[key] = (ref, ours, pwm.scales, pwm.codebook)
+    except TypeError:        # not weak-referenceable: no caching
+        pass
+    return ours
 
 
 def msgemm(pwm: PackedWeightMatrix, X, d: int, budget: int = DEFAULT_BUDGET,

@@ -90,3 +90,44 @@ def test_fast_path_rechecks_buffers():
         assert yv.shape == (512,) and yv.tobytes() == ypin.numpy()[:, 0].tobytes()
     with pytest.raises(ValueError):
         mg.msgemm(pwm, np.zeros(959, np.float16), 3)
+
+
+def test_foreign_weight_objects_are_wrapped_once():
+    """A reference-style PackedWeightMatrix (duck-typed: same fields, its own
+    Codebook / PerRow classes) is accepted and wrapped once, so repeated calls
+    reuse the repacked layout and call plans."""
+    from dataclasses import dataclass
+
+    @dataclass(frozen=True, eq=False)
+    class RefCodebook:
+        width: int
+        values: tuple
+
+    @dataclass(frozen=True, eq=False)
+    class RefPerRow:
+        q: np.ndarray
+
+    @dataclass(frozen=True, eq=False)
+    class RefPWM:
+        m: int
+        k: int
+        width: int
+        data: np.ndarray
+        codebook: RefCodebook
+        scales: object = None
+
+    rng = np.random.default_rng(9)
+    codes = rng.integers(0, 16, (300, 600), dtype=np.uint8)
+    ours = mg.from_codes(codes, mg.int4_codebook())
+    q = (rng.random(300) + 0.5).astype(np.float32)
+    ref = RefPWM(300, 600, 4, np.asarray(ours.data), RefCodebook(4, tuple(orc.int4_values().tolist())),
+                 RefPerRow(q))
+    X = rng.standard_normal((600, 4)).astype(np.float16)
+    y1 = mg.msgemm(ref, X, 3)
+    from paper_2310_06178_b200 import gemm
+    w1 = gemm._ensure_device_pwm(ref)
+    y2 = mg.msgemm(ref, X, 3)
+    assert gemm._ensure_device_pwm(ref) is w1
+    assert y1.tobytes() == y2.tobytes()
+    W = orc.int4_values()[codes] * q[:, None]
+    assert orc.rel_error(y1.astype(np.float64), W, X) <= 2e-3
