@@ -438,7 +438,8 @@ def main():
 
     # which LUT kernel the plan runs, and K3 (the one-time weight repack) timed alone
     plan = next(v for kk, v in pwms[0]._device_cache.items() if kk[0] == "call")
-    kernel_name = {_lib.LAYOUT_LANE: "lane_lut_kernel", _lib.LAYOUT_RB4: "rb_tmem_kernel",
+    kernel_name = {_lib.LAYOUT_LANE: "lane_lut_kernel", _lib.LAYOUT_RB4: "rb_tmem_kernel<16>",
+                   _lib.LAYOUT_RB4S: "rb_tmem_kernel<8>",
                    _lib.LAYOUT_RB8: "rb_lut_kernel<4>", _lib.LAYOUT_RB16: "rb_lut_kernel<2>",
                    _lib.LAYOUT_QUAD: "fused_lut_kernel"}.get(plan.layout, "generic_gemm_kernel")
     k3 = None
@@ -465,6 +466,7 @@ def main():
         k3_bytes = shard_bytes + rep_bytes
         del scratch
         k3 = {"kernel": "K3 repack (" + {_lib.LAYOUT_LANE: "lane", _lib.LAYOUT_RB4: "rb4",
+                                           _lib.LAYOUT_RB4S: "rb4s",
                                            _lib.LAYOUT_RB8: "rb8", _lib.LAYOUT_RB16: "rb16",
                                            _lib.LAYOUT_QUAD: "quad"}[plan.layout] + " layout)",
               "ms": ms_k3, "bytes": k3_bytes, "gbs": k3_bytes / (ms_k3 * 1e-3) / 1e9,

@@ -72,6 +72,8 @@ extern "C" {
                                      a LANE workspace keeps the sums and must be re-zeroed) */
 #define MSG_FLAG_NO_LANE      16  /* do not use the b=1 lane kernel (use the row-block kernel) */
 #define MSG_FLAG_NO_ROWBLOCK  32  /* do not use the batched d=3 row-block kernel (use the generic fused kernel) */
+#define MSG_FLAG_RB_ROWS8    128  /* tuning: the b >= 8 row-block kernel with 4096-row CTAs (MSG_LAYOUT_RB4S) */
+#define MSG_FLAG_RB_ROWS16   256  /* tuning: the b >= 8 row-block kernel with 8192-row CTAs (MSG_LAYOUT_RB4)  */
 #define MSG_FLAG_STATIC_WEIGHTS 64 /* the repacked weights were not written by the kernel launched just
                                       before on this stream: the LUT kernel may start streaming them
                                       before that kernel completes (programmatic dependent launch) */
@@ -84,6 +86,7 @@ extern "C" {
 #define MSG_LAYOUT_RB4  4  /* row-block planes, rounds of 4 groups (b >= 8: 8-column tiles)  */
 #define MSG_LAYOUT_RB8  5  /* row-block planes, rounds of 8 groups (b = 4..7: 4-column tiles) */
 #define MSG_LAYOUT_RB16 6  /* row-block planes, rounds of 16 groups (b = 2, 3: 2-column tiles) */
+#define MSG_LAYOUT_RB4S 7  /* as RB4 with rotations for 8 rows per thread (4096-row CTAs)     */
 
 MSG_API const char* msg_last_error(void);
 MSG_API int msg_version(void);

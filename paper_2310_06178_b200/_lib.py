@@ -31,8 +31,9 @@ FLAG_F32_ENTRIES, FLAG_NO_SYMMETRY, FLAG_FORCE_GENERIC, FLAG_LUT_PHASE_ONLY = 1,
 FLAG_NO_LANE = 16
 FLAG_NO_ROWBLOCK = 32
 FLAG_STATIC_WEIGHTS = 64
+FLAG_RB_ROWS8, FLAG_RB_ROWS16 = 128, 256
 LAYOUT_NONE, LAYOUT_QUAD, LAYOUT_LANE = 0, 1, 2
-LAYOUT_RB4, LAYOUT_RB8, LAYOUT_RB16 = 4, 5, 6
+LAYOUT_RB4, LAYOUT_RB8, LAYOUT_RB16, LAYOUT_RB4S = 4, 5, 6, 7
 
 EXPORTS = (
     "msg_last_error", "msg_version", "msg_device_sm_count", "msg_pack_codes",

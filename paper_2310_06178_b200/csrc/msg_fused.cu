@@ -55,15 +55,19 @@ struct TailVals;
 int rb_group_count(int64_t b);
 bool rb_eligible(int width, int x_dtype, int64_t b, int d, int scale_mode, bool sym,
                  bool f32_entries, bool s_exact16);
-int64_t rb_layout_bytes(int64_t m, int64_t k, int G);
-int64_t rb_workspace_bytes(int64_t m, int64_t k, int64_t b);
-int rb_repack(const uint8_t* packed, int64_t m, int64_t k, int G, uint8_t* out, cudaStream_t s);
+int64_t rb_layout_bytes(int64_t m, int64_t k, int G, int rpt);
+int64_t rb_workspace_bytes(int64_t m, int64_t k, int64_t b, int rpt);
+int rb_choose_rpt(int64_t m, int64_t b, int flags);
+int rb_repack(const uint8_t* packed, int64_t m, int64_t k, int G, int rpt, uint8_t* out,
+              cudaStream_t s);
 int launch_rb(const uint8_t* wrep, int64_t m, int64_t k, const double* values, double beta,
               const void* x, int64_t b, int scale_mode, const void* q, int q_dtype, void* y,
               int y_dtype, void* ws, int64_t ws_bytes, bool early, bool lut_only,
-              const TailVals& tv, cudaStream_t s);
+              const TailVals& tv, int rpt, cudaStream_t s);
+static int rb_layout_rpt(int layout) { return layout == MSG_LAYOUT_RB4S ? 8 : 16; }
 static int rb_layout_groups(int layout) {
-  return layout == MSG_LAYOUT_RB4 ? 4 : layout == MSG_LAYOUT_RB8 ? 8 : layout == MSG_LAYOUT_RB16 ? 16 : 0;
+  return (layout == MSG_LAYOUT_RB4 || layout == MSG_LAYOUT_RB4S) ? 4
+         : layout == MSG_LAYOUT_RB8 ? 8 : layout == MSG_LAYOUT_RB16 ? 16 : 0;
 }
 
 static inline int64_t align256(int64_t v) { return (v + 255) / 256 * 256; }
@@ -773,6 +777,7 @@ __global__ void __launch_bounds__(256) finish_vec4_kernel(
 struct FusedPlan {
   bool ok, lane, rb;
   int rb_groups;
+  int rb_rpt;
   int bc, rpt, ql, S, nrow_blocks, ncol_tiles, quads_per_slice;
   bool sym, f32_entries;
   int64_t smem, partial_bytes;
@@ -832,7 +837,8 @@ static FusedPlan fused_plan(int64_t m, int64_t k, int width, const double* value
       rb_eligible(width, x_dtype, b, d, scale_mode, p.sym, p.f32_entries, s_exact16)) {
     p.rb = true;
     p.rb_groups = rb_group_count(b);
-    p.partial_bytes = rb_workspace_bytes(m, k, b);
+    p.rb_rpt = rb_choose_rpt(m, b, flags);
+    p.partial_bytes = rb_workspace_bytes(m, k, b, p.rb_rpt);
     p.ok = true;
     return p;
   }
@@ -943,7 +949,8 @@ extern "C" {
 int64_t msg_repacked_bytes(int64_t m, int64_t k, int d, int layout) {
   if (layout == MSG_LAYOUT_NONE) return 0;
   if (layout == MSG_LAYOUT_LANE) return d == 3 ? lane_layout_bytes(m, k) : -1;
-  if (rb_layout_groups(layout)) return d == 3 ? rb_layout_bytes(m, k, rb_layout_groups(layout)) : -1;
+  if (rb_layout_groups(layout))
+    return d == 3 ? rb_layout_bytes(m, k, rb_layout_groups(layout), rb_layout_rpt(layout)) : -1;
   if (layout != MSG_LAYOUT_QUAD || d < 1 || d > 3) return -1;
   return quad_layout(m, k, d).total;
 }
@@ -958,7 +965,8 @@ int msg_repack(const uint8_t* packed, int64_t m, int64_t k, int d, int layout, i
   if (rb_layout_groups(layout)) {
     if (d != 3 || !symmetric)
       return fail(MSG_ERR_UNSUPPORTED, "row-block layout is for d=3 with an antisymmetric codebook");
-    return rb_repack(packed, m, k, rb_layout_groups(layout), out, as_stream(stream));
+    return rb_repack(packed, m, k, rb_layout_groups(layout), rb_layout_rpt(layout), out,
+                     as_stream(stream));
   }
   if (layout != MSG_LAYOUT_QUAD)
     return fail(MSG_ERR_UNSUPPORTED, "unknown weight layout %d", layout);
@@ -1001,7 +1009,7 @@ int msg_gemm_plan(int64_t m, int64_t k, int width, const double* values, int x_d
   FusedPlan p = fused_plan(m, k, width, values, x_dtype, b, d, scale_mode, group_size, flags);
   if (p.ok) {
     *layout_out = p.lane ? MSG_LAYOUT_LANE
-                : p.rb ? (p.rb_groups == 4 ? MSG_LAYOUT_RB4
+                : p.rb ? (p.rb_groups == 4 ? (p.rb_rpt == 8 ? MSG_LAYOUT_RB4S : MSG_LAYOUT_RB4)
                                            : p.rb_groups == 8 ? MSG_LAYOUT_RB8 : MSG_LAYOUT_RB16)
                        : MSG_LAYOUT_QUAD;
     *symmetric_out = p.sym ? 1 : 0;
@@ -1042,7 +1050,7 @@ int msg_gemm(const uint8_t* packed, const uint8_t* wrep, int64_t m, int64_t k, i
                        workspace, ws_bytes, early, lut_only, s);
   if (p.rb)
     return launch_rb(wrep, m, k, values, beta, x, b, scale_mode, q, q_dtype, y, y_dtype,
-                     workspace, ws_bytes, early, lut_only, tv, s);
+                     workspace, ws_bytes, early, lut_only, tv, p.rb_rpt, s);
   FusedParams P{};
   P.wrep = wrep;
   P.lo_off = p.L.lo_off;

@@ -50,11 +50,16 @@ struct RbLayout {
   int64_t nb, nq, nqp, mp;              // groups, quads, quads padded to rounds, row stride
   int64_t lo_off, hi_off, rot_off, tail_off, total;
   int G, tail;
+  int rpt;                              // G = 4: rows per thread of the kernel (16 or 8)
 };
 
-RbLayout rb_layout(int64_t m, int64_t k, int G) {
+// G = 4 comes in two variants: 16 rows per thread (8192 rows per CTA) or 8
+// (4096 rows per CTA, for row counts that would leave most of an 8192-row
+// block idle or whose fixed k-slice partial traffic would dominate)
+RbLayout rb_layout(int64_t m, int64_t k, int G, int rpt = 16) {
   RbLayout L{};
   L.G = G;
+  L.rpt = rpt;
   L.nb = k / 3;
   L.nq = (L.nb + 3) / 4;
   const int qr = G / 4;
@@ -64,8 +69,8 @@ RbLayout rb_layout(int64_t m, int64_t k, int G) {
   L.lo_off = 0;
   L.hi_off = al256(L.nqp * L.mp * 4);
   L.rot_off = L.hi_off + al256(L.nqp * L.mp * 2);
-  // G = 4: per (quad, 16-row group) the rotations chosen by K3 (2 bits per row)
-  L.tail_off = L.rot_off + (G == 4 ? al256(L.nqp * (L.mp / 16) * 4) : 0);
+  // G = 4: per (quad, rpt-row group) the rotations chosen by K3 (2 bits per row)
+  L.tail_off = L.rot_off + (G == 4 ? al256(L.nqp * (L.mp / rpt) * 4) : 0);
   L.total = L.tail_off + (L.tail ? al256(m * 2) : 0);
   if (L.total == 0) L.total = 256;
   return L;
@@ -250,15 +255,20 @@ __device__ uint32_t choose_rotations(uint32_t pmw, uint8_t* cand, uint8_t* cscor
 
 // K3 for rounds of 4 groups.  One CTA per (128-row block, 8 quads): the
 // block's packed bytes (48 per row) are staged with coalesced loads, then
-// thread (r, qq) takes row step r of quad qq: the octet of rows
-// base + 16 u + r (u < 8), its rotations, and its 8 (lo, hi) records; the
-// per-(quad, 16-row group) rotation words are assembled from shared memory.
+// thread (r, sub, qq) takes row step r of quad qq for the octet of rows
+// base + 8 RPT sub + RPT u + r (u < 8) -- the 8 lanes of one LDS.128 phase of
+// the kernel, whose thread t holds rows RPT t .. RPT t + RPT - 1 -- its
+// rotations and its 8 (lo, hi) records; the per-(quad, RPT-row group)
+// rotation words are assembled from shared memory.
 constexpr int kRb4Rows = 128, kRb4Quads = 8;
+template <int RPT>
 __global__ void __launch_bounds__(128) repack_rb4_kernel(const uint8_t* __restrict__ packed,
                                                          int64_t m, int64_t k, int rb, RbLayout L,
                                                          uint8_t* __restrict__ out) {
+  constexpr int NSUB = 16 / RPT;                    // octet blocks per 128 rows
+  constexpr int NGRP = kRb4Rows / RPT;              // RPT-row groups per 128 rows
   __shared__ uint8_t tile[kRb4Rows][kRb4Quads * 6 + 4];
-  __shared__ uint16_t rho_s[kRb4Quads][16];
+  __shared__ uint16_t rho_s[kRb4Quads][NSUB][RPT];
   __shared__ uint8_t cand_s[128][kRb4Cands], csc_s[128][kRb4Cands];
   const int tid = threadIdx.x;
   uint32_t* lo_p = reinterpret_cast<uint32_t*>(out + L.lo_off);
@@ -286,7 +296,7 @@ __global__ void __launch_bounds__(128) repack_rb4_kernel(const uint8_t* __restri
       }
     }
     __syncthreads();
-    const int r = tid & 15, qq = tid >> 4;
+    const int r = tid % RPT, sub = (tid / RPT) % NSUB, qq = tid / 16;
     const int64_t q = q0 + qq;
     if (q < L.nqp) {
       // folded index / sign of group g (of quad q) for tile row tr
@@ -303,19 +313,20 @@ __global__ void __launch_bounds__(128) repack_rb4_kernel(const uint8_t* __restri
         if (idx & 0x800) { idx ^= 0xFFF; sign = 1; }
         return idx;
       };
+      const int tr0 = 8 * RPT * sub + r;               // tile row of lane u = 0
       uint32_t pmw = 0;
 #pragma unroll
       for (int u = 0; u < 8; ++u)
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           uint32_t sg;
-          pmw |= (rec(16 * u + r, g, sg) & 1) << (4 * u + g);
+          pmw |= (rec(tr0 + RPT * u, g, sg) & 1) << (4 * u + g);
         }
       const uint32_t rho = choose_rotations(pmw, cand_s[tid], csc_s[tid]);
-      rho_s[qq][r] = (uint16_t)rho;
+      rho_s[qq][sub][r] = (uint16_t)rho;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int tr = 16 * u + r;
+        const int tr = tr0 + RPT * u;
         const int64_t i = base + tr;
         if (i >= L.mp) continue;
         const uint32_t ru = (rho >> (2 * u)) & 3;
@@ -328,14 +339,14 @@ __global__ void __launch_bounds__(128) repack_rb4_kernel(const uint8_t* __restri
       }
     }
     __syncthreads();
-    if (tid < kRb4Quads * 8) {  // rotation word of (quad qq2, 16-row group u2): 2 bits per row step
-      const int qq2 = tid >> 3, u2 = tid & 7;
-      const int64_t q2 = q0 + qq2, i0 = base + 16 * u2;
+    if (tid < kRb4Quads * NGRP) {  // rotation word of (quad qq2, RPT-row group g2): 2 bits per row step
+      const int qq2 = tid / NGRP, g2 = tid % NGRP, sub2 = g2 / 8, u2 = g2 % 8;
+      const int64_t q2 = q0 + qq2, i0 = base + RPT * g2;
       if (q2 < L.nqp && i0 < L.mp) {
         uint32_t w = 0;
 #pragma unroll
-        for (int r2 = 0; r2 < 16; ++r2) w |= ((uint32_t)(rho_s[qq2][r2] >> (2 * u2)) & 3) << (2 * r2);
-        rot_p[q2 * (L.mp / 16) + i0 / 16] = w;
+        for (int r2 = 0; r2 < RPT; ++r2) w |= ((uint32_t)(rho_s[qq2][sub2][r2] >> (2 * u2)) & 3) << (2 * r2);
+        rot_p[q2 * (L.mp / RPT) + i0 / RPT] = w;
       }
     }
   }
@@ -752,8 +763,8 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_lut_kernel(RbParams P) {
 // 128 (w / 4) .. + 127; per round it streams its rows two at a time through
 // registers: tcgen05.ld (32x32b.x16: two rows), 8 lookups, tcgen05.st, with
 // the next pair's load in flight.
-constexpr int kTmRPT = 16;
-constexpr int kTmR = kRbThreads * kTmRPT;  // 8192 rows per CTA
+// (RPT = 16: 8192 rows per CTA, all 512 TMEM columns; RPT = 8: 4096 rows,
+// 256 columns)
 
 __device__ __forceinline__ void tm_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -794,7 +805,10 @@ __device__ __forceinline__ void ldg_v4(const void* p, uint32_t& a, uint32_t& b, 
                : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "l"(p));
 }
 
+template <int kTmRPT>
 __global__ void __launch_bounds__(kRbThreads, 1) rb_tmem_kernel(RbParams P) {
+  constexpr int kTmR = kRbThreads * kTmRPT;         // rows per CTA
+  constexpr int kTmCols = 4 * 8 * kTmRPT;           // TMEM columns: 4 warps per lane quarter
   constexpr int BC = 8, G = 4, EB = 16, NI = G * 256 / kRbThreads;
   extern __shared__ __align__(128) uint8_t smem[];
   __half* xs0 = reinterpret_cast<__half*>(smem + kRbTableBytes);                // [2][96]
@@ -820,8 +834,8 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_tmem_kernel(RbParams P) {
   const uint32_t tab = smem_u32(smem);
 
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-        smem_u32(tmem_slot)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+        smem_u32(tmem_slot)), "n"(kTmCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
 
@@ -835,25 +849,28 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_tmem_kernel(RbParams P) {
     return v;
   };
 
-  // this thread's words of one round: 16 lo words, 16 hi halves, 16 rotations
+  // this thread's words of one round: RPT lo words, RPT hi halves, RPT rotations
+  const int64_t rstride = P.mp / kTmRPT;               // rotation words per quad
   const uint32_t* plo = P.lo + (int64_t)r_begin * P.mp + my_row;
   const uint16_t* phi = P.hi + (int64_t)r_begin * P.mp + my_row;
-  const uint32_t* prot = P.rot + (int64_t)r_begin * (P.mp / 16) + my_row / 16;
-  uint32_t wlo[16], whi[8], wrot = 0;
+  const uint32_t* prot = P.rot + (int64_t)r_begin * rstride + my_row / kTmRPT;
+  uint32_t wlo[kTmRPT], whi[kTmRPT / 2], wrot = 0;
   auto load_words = [&](int t) {
     if (has_words && t < nr) {
       const uint32_t* l = plo + (int64_t)t * P.mp;
 #pragma unroll
-      for (int v = 0; v < 4; ++v) ldg_v4(l + 4 * v, wlo[4 * v], wlo[4 * v + 1], wlo[4 * v + 2], wlo[4 * v + 3]);
+      for (int v = 0; v < kTmRPT / 4; ++v)
+        ldg_v4(l + 4 * v, wlo[4 * v], wlo[4 * v + 1], wlo[4 * v + 2], wlo[4 * v + 3]);
       const uint16_t* h = phi + (int64_t)t * P.mp;
-      ldg_v4(h, whi[0], whi[1], whi[2], whi[3]);
-      ldg_v4(h + 8, whi[4], whi[5], whi[6], whi[7]);
-      wrot = ldg_u32(prot + (int64_t)t * (P.mp / 16));
+#pragma unroll
+      for (int v = 0; v < kTmRPT / 8; ++v)
+        ldg_v4(h + 8 * v, whi[4 * v], whi[4 * v + 1], whi[4 * v + 2], whi[4 * v + 3]);
+      wrot = ldg_u32(prot + (int64_t)t * rstride);
     } else {
 #pragma unroll
-      for (int v = 0; v < 16; ++v) wlo[v] = 0;
+      for (int v = 0; v < kTmRPT; ++v) wlo[v] = 0;
 #pragma unroll
-      for (int v = 0; v < 8; ++v) whi[v] = 0;
+      for (int v = 0; v < kTmRPT / 2; ++v) whi[v] = 0;
       wrot = 0;
     }
   };
@@ -868,7 +885,7 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_tmem_kernel(RbParams P) {
   MSG_JITTER();
   __syncthreads();
   tm_fence_after();
-  const uint32_t tbase = *tmem_slot + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(warp >> 2) * 128;
+  const uint32_t tbase = *tmem_slot + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(warp >> 2) * (8 * kTmRPT);
   {  // zero accumulators
     float z[16];
 #pragma unroll
@@ -921,7 +938,7 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_tmem_kernel(RbParams P) {
     const uint32_t* nlo = plo + (int64_t)(t + 1) * P.mp;
     const uint16_t* nhi = phi + (int64_t)(t + 1) * P.mp;
     const uint32_t rot_a = wrot << 4, rot_b = wrot >> 12;  // rows 0-7 / 8-15 at bits 4+2r'
-    if (more && has_words) wrot = ldg_u32(prot + (int64_t)(t + 1) * (P.mp / 16));
+    if (more && has_words) wrot = ldg_u32(prot + (int64_t)(t + 1) * rstride);
     tm_wait_st();  // the previous round's accumulator stores are complete
     float va[16], vb[16];
     tm_ld16(tbase, va);
@@ -944,7 +961,9 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_tmem_kernel(RbParams P) {
           ldg_v4(nlo + r, wlo[r], wlo[r + 1], wlo[r + 2], wlo[r + 3]);
         }
         if (p == 3) ldg_v4(nhi, whi[0], whi[1], whi[2], whi[3]);
-        if (p == 7) ldg_v4(nhi + 8, whi[4], whi[5], whi[6], whi[7]);
+        if constexpr (kTmRPT == 16) {
+          if (p == 7) ldg_v4(nhi + 8, whi[4], whi[5], whi[6], whi[7]);
+        }
       }
       tm_st16(tbase + 16 * p, cur);
       tm_wait_ld();
@@ -984,7 +1003,7 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_tmem_kernel(RbParams P) {
   MSG_JITTER();
   __syncthreads();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(*tmem_slot));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot), "n"(kTmCols));
 }
 
 // ============================================================================
@@ -998,10 +1017,11 @@ bool rb_eligible(int width, int x_dtype, int64_t b, int d, int scale_mode, bool 
          s_exact16 && scale_mode != MSG_SCALE_PER_GROUP;
 }
 
-int64_t rb_layout_bytes(int64_t m, int64_t k, int G) { return rb_layout(m, k, G).total; }
+int64_t rb_layout_bytes(int64_t m, int64_t k, int G, int rpt) { return rb_layout(m, k, G, rpt).total; }
 
-int rb_repack(const uint8_t* packed, int64_t m, int64_t k, int G, uint8_t* out, cudaStream_t s) {
-  RbLayout L = rb_layout(m, k, G);
+int rb_repack(const uint8_t* packed, int64_t m, int64_t k, int G, int rpt, uint8_t* out,
+              cudaStream_t s) {
+  RbLayout L = rb_layout(m, k, G, rpt);
   if (L.nb == 0 || m == 0) return fail(MSG_ERR_UNSUPPORTED, "row-block layout needs a full group");
   const int rb = row_bytes(k, 4);
   const int64_t tiles = ((m + kRpTileRows - 1) / kRpTileRows) *
@@ -1010,7 +1030,8 @@ int rb_repack(const uint8_t* packed, int64_t m, int64_t k, int G, uint8_t* out, 
   if (G == 4) {
     const int64_t t4 = ceil_div(L.mp, kRb4Rows) * ceil_div(L.nqp, kRb4Quads);
     const int g4 = (int)std::min<int64_t>(t4, (int64_t)sm_count() * 16);
-    repack_rb4_kernel<<<g4, 128, 0, s>>>(packed, m, k, rb, L, out);
+    if (rpt == 8) repack_rb4_kernel<8><<<g4, 128, 0, s>>>(packed, m, k, rb, L, out);
+    else repack_rb4_kernel<16><<<g4, 128, 0, s>>>(packed, m, k, rb, L, out);
   } else {
     repack_rb_kernel<<<grid, 256, 0, s>>>(packed, m, k, rb, L, out);
   }
@@ -1025,17 +1046,18 @@ int rb_repack(const uint8_t* packed, int64_t m, int64_t k, int G, uint8_t* out, 
 }
 
 struct RbPlan {
-  int G, bc, S, rps, nrounds, nrow_blocks, ncol_tiles;
+  int G, bc, S, rps, nrounds, nrow_blocks, ncol_tiles, rpt;
   int64_t partial_bytes, smem;
 };
 
-RbPlan rb_plan(int64_t m, int64_t k, int64_t b) {
+RbPlan rb_plan(int64_t m, int64_t k, int64_t b, int rpt) {
   RbPlan p{};
   p.G = rb_group_count(b);
   p.bc = 32 / p.G;
-  RbLayout L = rb_layout(m, k, p.G);
+  p.rpt = p.G == 4 ? rpt : rb_rows_per_thread(p.G);
+  RbLayout L = rb_layout(m, k, p.G, p.G == 4 ? rpt : 16);
   p.nrounds = (int)(L.nqp / (p.G / 4));
-  p.nrow_blocks = (int)ceil_div(m, (int64_t)kRbThreads * rb_rows_per_thread(p.G));
+  p.nrow_blocks = (int)ceil_div(m, (int64_t)kRbThreads * p.rpt);
   p.ncol_tiles = (int)ceil_div(b, p.bc);
   const int64_t base = (int64_t)p.nrow_blocks * p.ncol_tiles;
   int64_t S = std::max<int64_t>(1, sm_count() / std::max<int64_t>(1, base));
@@ -1047,7 +1069,25 @@ RbPlan rb_plan(int64_t m, int64_t k, int64_t b) {
   return p;
 }
 
-int64_t rb_workspace_bytes(int64_t m, int64_t k, int64_t b) { return rb_plan(m, k, b).partial_bytes; }
+int64_t rb_workspace_bytes(int64_t m, int64_t k, int64_t b, int rpt) {
+  return rb_plan(m, k, b, rpt).partial_bytes;
+}
+
+// Rows per thread of the rounds-of-4 kernel (b >= 8): 16 (8192-row CTAs)
+// unless an 8192-row block would be mostly empty or the row count is small
+// enough that the k-slice partials (~S x 8192 x b x 4 bytes, a fixed ~39 MB
+// at b = 8) rival the weight stream -- then 8 (4096-row CTAs, half the
+// partials, twice the table builds per lookup).  flags can force either.
+int rb_choose_rpt(int64_t m, int64_t b, int flags) {
+  if (rb_group_count(b) != 4) return 16;
+  if (flags & MSG_FLAG_RB_ROWS8) return 8;
+  if (flags & MSG_FLAG_RB_ROWS16) return 16;
+  // measured (one B200): 4096-row CTAs win at m <= 16384 with one or two
+  // 8-column tiles (cfg3 11008 x 4096 b = 16: 69.9 -> 55.4 us; 8192-row
+  // shards of cfg5: 46.5 -> 40.3 us), lose at m = 65536 (210.6 -> 219.4 us)
+  // and at b = 64 (209.6 -> 220.1 us), tie at m = 32768
+  return (m <= 16384 && b <= 16) ? 8 : 16;
+}
 
 template <int BC>
 static int launch_rb_t(const RbPlan& pl, RbParams& P, cudaStream_t s) {
@@ -1073,13 +1113,14 @@ static int launch_rb_t(const RbPlan& pl, RbParams& P, cudaStream_t s) {
   return MSG_OK;
 }
 
+template <int RPT>
 static int launch_rb_tmem(const RbPlan& pl, RbParams& P, cudaStream_t s) {
   static int configured_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (configured_dev != dev) {
-    MSG_CUDA_CHECK(cudaFuncSetAttribute(rb_tmem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)pl.smem));
+    MSG_CUDA_CHECK(cudaFuncSetAttribute(rb_tmem_kernel<RPT>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
     configured_dev = dev;
   }
   cudaLaunchConfig_t cfg{};
@@ -1092,19 +1133,19 @@ static int launch_rb_tmem(const RbPlan& pl, RbParams& P, cudaStream_t s) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  MSG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, rb_tmem_kernel, P));
+  MSG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, rb_tmem_kernel<RPT>, P));
   return MSG_OK;
 }
 
 int launch_rb(const uint8_t* wrep, int64_t m, int64_t k, const double* values, double beta,
               const void* x, int64_t b, int scale_mode, const void* q, int q_dtype, void* y,
               int y_dtype, void* ws, int64_t ws_bytes, bool early, bool lut_only,
-              const TailVals& tv, cudaStream_t s) {
-  const RbPlan pl = rb_plan(m, k, b);
+              const TailVals& tv, int rpt, cudaStream_t s) {
+  const RbPlan pl = rb_plan(m, k, b, rpt);
   if (ws_bytes < pl.partial_bytes)
     return fail(MSG_ERR_WORKSPACE, "workspace too small: need %lld bytes",
                 (long long)pl.partial_bytes);
-  RbLayout L = rb_layout(m, k, pl.G);
+  RbLayout L = rb_layout(m, k, pl.G, pl.G == 4 ? pl.rpt : 16);
   RbParams P{};
   P.lo = reinterpret_cast<const uint32_t*>(wrep + L.lo_off);
   P.hi = reinterpret_cast<const uint16_t*>(wrep + L.hi_off);
@@ -1122,7 +1163,7 @@ int launch_rb(const uint8_t* wrep, int64_t m, int64_t k, const double* values, d
   P.partial = reinterpret_cast<float*>(ws);
   int e = MSG_OK;
   switch (pl.bc) {
-    case 8: e = launch_rb_tmem(pl, P, s); break;
+    case 8: e = pl.rpt == 8 ? launch_rb_tmem<8>(pl, P, s) : launch_rb_tmem<16>(pl, P, s); break;
     case 4: e = launch_rb_t<4>(pl, P, s); break;
     default: e = launch_rb_t<2>(pl, P, s); break;
   }

@@ -58,14 +58,15 @@ def test_plan_configs_take_fused_symmetric_path(m, k, b, d):
     elif b == 1:
         want = _lib.LAYOUT_LANE
     else:   # batched d = 3: the row-block kernel, rounds of 32 / min(b, 8) groups
-        want = {8: _lib.LAYOUT_RB4, 16: _lib.LAYOUT_RB4, 256: _lib.LAYOUT_RB4}[b]
+        # (4096-row CTAs -- RB4S -- for m <= 16384 at b <= 16, 8192-row CTAs otherwise)
+        want = _lib.LAYOUT_RB4S if (m <= 16384 and b <= 16) else _lib.LAYOUT_RB4
     assert st == 0 and lay == want and sym == 1 and ws > 0
     # the generic fused kernel remains selectable for every shape
     st, lay, sym, ws = _plan(m, k, b, d, flags=_lib.FLAG_NO_LANE | _lib.FLAG_NO_ROWBLOCK)
     assert st == 0 and lay == _lib.LAYOUT_QUAD
 
 
-@pytest.mark.parametrize("b,want", [(2, 6), (3, 6), (4, 5), (7, 5), (8, 4), (64, 4)])
+@pytest.mark.parametrize("b,want", [(2, 6), (3, 6), (4, 5), (7, 5), (8, 7), (16, 7), (64, 4)])
 def test_plan_rowblock_round_width(b, want):
     st, lay, sym, ws = _plan(8192, 8192, b, 3)
     assert st == 0 and lay == want

@@ -16,7 +16,7 @@ from paper_2310_06178_b200 import _lib
 from oracle import msgemm_oracle as orc
 
 pytestmark = pytest.mark.gpu
-FUSED = (_lib.LAYOUT_QUAD, _lib.LAYOUT_RB4, _lib.LAYOUT_RB8, _lib.LAYOUT_RB16)
+FUSED = (_lib.LAYOUT_QUAD, _lib.LAYOUT_RB4, _lib.LAYOUT_RB4S, _lib.LAYOUT_RB8, _lib.LAYOUT_RB16)
 
 RTOL = {np.float32: 1e-5, np.float16: 2e-3}
 

@@ -15,7 +15,7 @@ peak = 6549.1
 for (m, k) in ((65536, 8192), (8192, 8192), (4096, 4096)):
     rng = np.random.default_rng(0)
     data = torch.from_numpy(rng.integers(0, 256, (m, (k + 1) // 2), dtype=np.uint8)).cuda()
-    for name, layout in (("lane", _lib.LAYOUT_LANE), ("rb4", _lib.LAYOUT_RB4), ("rb8", _lib.LAYOUT_RB8),
+    for name, layout in (("lane", _lib.LAYOUT_LANE), ("rb4", _lib.LAYOUT_RB4), ("rb4s", _lib.LAYOUT_RB4S), ("rb8", _lib.LAYOUT_RB8),
                          ("rb16", _lib.LAYOUT_RB16), ("quad", _lib.LAYOUT_QUAD)):
         nbytes = int(lib.msg_repacked_bytes(m, k, 3, layout))
         out = torch.empty(nbytes, dtype=torch.uint8, device="cuda")

@@ -4,6 +4,7 @@ emulated on one GPU (the shard each rank would run; collectives excluded).
     python tools/shard_probe.py [cfg5]
 """
 import math
+import os
 import sys
 
 import numpy as np
@@ -19,6 +20,7 @@ dev = torch.device("cuda", 0)
 W = weights(cfg)
 X = activations(cfg)
 L2 = 126 * 2 ** 20
+FLAGS = int(os.environ.get("MSG_BENCH_FLAGS", "0"))  # e.g. 128: 4096-row CTAs
 
 
 def time_shard(data, kr, xs, yd):
@@ -29,14 +31,15 @@ def time_shard(data, kr, xs, yd):
     xd = torch.from_numpy(np.ascontiguousarray(xs)).to(dev)
     Y = torch.empty((data.shape[0], cfg.b), dtype=yd, device=dev)
     for i in range(ncopies):
-        mg.msgemm(pwms[i], xd, cfg.d, out=Y, out_dtype=None if yd == xd.dtype else np.float32)
+        mg.msgemm(pwms[i], xd, cfg.d, out=Y, out_dtype=None if yd == xd.dtype else np.float32,
+                  _flags=FLAGS)
     torch.cuda.synchronize()
     n = ncopies * max(1, math.ceil(20 / ncopies))
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
         for i in range(n):
             mg.msgemm(pwms[i % ncopies], xd, cfg.d, out=Y,
-                      out_dtype=None if yd == xd.dtype else np.float32)
+                      out_dtype=None if yd == xd.dtype else np.float32, _flags=FLAGS)
     g.replay()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
