@@ -17,9 +17,9 @@ full() {  # config kernel-regex name
   ncu --set full --clock-control none --import-source on -k regex:$2 -s 2 -c 1 \
       -o $O/full_$3 $B --config $1 > /dev/null 2>&1
 }
-full cfg5 rb_tmem cfg5_rb_tmem
+full cfg5 rb_tmem cfg5_rb_tmem16
+full cfg3 rb_tmem cfg3_rb_tmem8
 full cfg4b1 lane_lut cfg4b1_lane_lut
-full cfg4b1 dq_mma cfg4b1_dq_mma
+full cfg4b1 dq_gemv cfg4b1_dq_gemv
 full cfg4b256 dq_mma cfg4b256_dq_mma
-full cfg4b16 rb_tmem cfg4b16_rb_tmem
 ls -la $O
