@@ -200,27 +200,78 @@ constexpr int kRb4Cands = 4;  // pairings searched (simulated: top-4 matches top
 // equal-parity (pair, table) incidences are searched over the 24 rotation
 // permutations (ties: earlier pairings first); cand/cscore are this thread's
 // slots in shared memory (dynamically indexed, so not in registers).
-__device__ uint32_t choose_rotations(uint32_t pmw, uint8_t* cand, uint8_t* cscore) {
-  int nc = 0;
-  for (int p = 0; p < 105; ++p) {
-    const uint32_t code = kPairings[p];
-    int sc = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t a = (code >> (8 * i)) & 0xF, b = (code >> (8 * i + 4)) & 0xF;
-      sc += __popc(~((pmw >> (4 * a)) ^ (pmw >> (4 * b))) & 0xF);
-    }
-    if (nc < kRb4Cands || sc < cscore[nc - 1]) {  // keep the best (stable: earlier first)
+// the 4 lane pairs of every pairing as indices into the 28 pairs (a < b),
+// pair (a, b) -> a (15 - a) / 2 + b - a - 1 (compile-time copy of kPairings)
+__host__ __device__ constexpr int pair_idx(int p, int i) {
+  constexpr uint8_t t[105][4] = {
+    {0, 13, 22, 27}, {0, 13, 23, 26}, {0, 13, 24, 25}, {0, 14, 19, 27}, {0, 14, 20, 26}, {0, 14, 21, 25},
+    {0, 15, 18, 27}, {0, 15, 20, 24}, {0, 15, 21, 23}, {0, 16, 18, 26}, {0, 16, 19, 24}, {0, 16, 21, 22},
+    {0, 17, 18, 25}, {0, 17, 19, 23}, {0, 17, 20, 22}, {1, 8, 22, 27}, {1, 8, 23, 26}, {1, 8, 24, 25},
+    {1, 9, 19, 27}, {1, 9, 20, 26}, {1, 9, 21, 25}, {1, 10, 18, 27}, {1, 10, 20, 24}, {1, 10, 21, 23},
+    {1, 11, 18, 26}, {1, 11, 19, 24}, {1, 11, 21, 22}, {1, 12, 18, 25}, {1, 12, 19, 23}, {1, 12, 20, 22},
+    {2, 7, 22, 27}, {2, 7, 23, 26}, {2, 7, 24, 25}, {2, 9, 15, 27}, {2, 9, 16, 26}, {2, 9, 17, 25},
+    {2, 10, 14, 27}, {2, 10, 16, 24}, {2, 10, 17, 23}, {2, 11, 14, 26}, {2, 11, 15, 24}, {2, 11, 17, 22},
+    {2, 12, 14, 25}, {2, 12, 15, 23}, {2, 12, 16, 22}, {3, 7, 19, 27}, {3, 7, 20, 26}, {3, 7, 21, 25},
+    {3, 8, 15, 27}, {3, 8, 16, 26}, {3, 8, 17, 25}, {3, 10, 13, 27}, {3, 10, 16, 21}, {3, 10, 17, 20},
+    {3, 11, 13, 26}, {3, 11, 15, 21}, {3, 11, 17, 19}, {3, 12, 13, 25}, {3, 12, 15, 20}, {3, 12, 16, 19},
+    {4, 7, 18, 27}, {4, 7, 20, 24}, {4, 7, 21, 23}, {4, 8, 14, 27}, {4, 8, 16, 24}, {4, 8, 17, 23},
+    {4, 9, 13, 27}, {4, 9, 16, 21}, {4, 9, 17, 20}, {4, 11, 13, 24}, {4, 11, 14, 21}, {4, 11, 17, 18},
+    {4, 12, 13, 23}, {4, 12, 14, 20}, {4, 12, 16, 18}, {5, 7, 18, 26}, {5, 7, 19, 24}, {5, 7, 21, 22},
+    {5, 8, 14, 26}, {5, 8, 15, 24}, {5, 8, 17, 22}, {5, 9, 13, 26}, {5, 9, 15, 21}, {5, 9, 17, 19},
+    {5, 10, 13, 24}, {5, 10, 14, 21}, {5, 10, 17, 18}, {5, 12, 13, 22}, {5, 12, 14, 19}, {5, 12, 15, 18},
+    {6, 7, 18, 25}, {6, 7, 19, 23}, {6, 7, 20, 22}, {6, 8, 14, 25}, {6, 8, 15, 23}, {6, 8, 16, 22},
+    {6, 9, 13, 25}, {6, 9, 15, 20}, {6, 9, 16, 19}, {6, 10, 13, 23}, {6, 10, 14, 20}, {6, 10, 16, 18},
+    {6, 11, 13, 22}, {6, 11, 14, 19}, {6, 11, 15, 18}};
+  return t[p][i];
+}
+__host__ __device__ constexpr uint32_t perm_code(int q) {
+  constexpr uint8_t t[24] = {0xe4, 0xb4, 0xd8, 0x78, 0x9c, 0x6c, 0xe1, 0xb1, 0xc9, 0x39, 0x8d, 0x2d, 0xd2, 0x72, 0xc6, 0x36, 0x4e, 0x1e, 0x93, 0x63, 0x87, 0x27, 0x4b, 0x1b};
+  return t[q];
+}
+
+// pairing P's score (equal-parity incidences) into the running top-K; template
+// recursion so every pair index is a compile-time constant (pc stays in registers)
+template <int P>
+__device__ __forceinline__ void score_pairings(const int (&pc)[28], int& nc, int& worst, uint8_t* cand,
+                                               uint8_t* cscore) {
+  if constexpr (P < 105) {
+    const int sc = pc[pair_idx(P, 0)] + pc[pair_idx(P, 1)] + pc[pair_idx(P, 2)] + pc[pair_idx(P, 3)];
+    if (nc < kRb4Cands || sc < worst) {  // keep the best (stable: earlier first)
       int pos = nc < kRb4Cands ? nc++ : kRb4Cands - 1;
       while (pos > 0 && cscore[pos - 1] > sc) {
         cand[pos] = cand[pos - 1];
         cscore[pos] = cscore[pos - 1];
         --pos;
       }
-      cand[pos] = (uint8_t)p;
+      cand[pos] = (uint8_t)P;
       cscore[pos] = (uint8_t)sc;
+      worst = nc < kRb4Cands ? 99 : cscore[kRb4Cands - 1];
     }
+    score_pairings<P + 1>(pc, nc, worst, cand, cscore);
   }
+}
+
+template <int Q>
+__device__ __forceinline__ void best_perm(const uint32_t (&rm)[4], int& cbest, int& qbest) {
+  if constexpr (Q < 24) {
+    constexpr uint32_t pr = perm_code(Q);
+    const uint32_t u = (rm[0] >> (4 * (pr & 3))) | (rm[1] >> (4 * ((pr >> 2) & 3))) |
+                       (rm[2] >> (4 * ((pr >> 4) & 3))) | (rm[3] >> (4 * (pr >> 6)));
+    const int cost = __popc(u & 0xF);
+    if (cost < cbest) { cbest = cost; qbest = Q; }
+    best_perm<Q + 1>(rm, cbest, qbest);
+  }
+}
+
+__device__ uint32_t choose_rotations(uint32_t pmw, uint8_t* cand, uint8_t* cscore) {
+  // equal-parity count of every lane pair, once (the 105 pairings reuse them)
+  int pc[28];
+#pragma unroll
+  for (int a = 0, n = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = a + 1; b < 8; ++b, ++n) pc[n] = __popc(~((pmw >> (4 * a)) ^ (pmw >> (4 * b))) & 0xF);
+  int nc = 0, worst = 99;
+  score_pairings<0>(pc, nc, worst, cand, cscore);
   int best = 99;
   uint32_t best_rho = 0;
   for (int c = 0; c < nc; ++c) {
@@ -232,22 +283,19 @@ __device__ uint32_t choose_rotations(uint32_t pmw, uint8_t* cand, uint8_t* cscor
       const uint32_t bad = ~((pmw >> (4 * a)) ^ (pmw >> (4 * b))) & 0xF;
       rm[i] = bad | (rotr4(bad, 1) << 4) | (rotr4(bad, 2) << 8) | (rotr4(bad, 3) << 12);
     }
-    for (int q = 0; q < 24; ++q) {
-      const uint32_t pr = kPerms[q];
-      const uint32_t u = (rm[0] >> (4 * (pr & 3))) | (rm[1] >> (4 * ((pr >> 2) & 3))) |
-                         (rm[2] >> (4 * ((pr >> 4) & 3))) | (rm[3] >> (4 * (pr >> 6)));
-      const int cost = __popc(u & 0xF);
-      if (cost < best) {
-        best = cost;
-        uint32_t rho = 0;
+    int cbest = 99, qbest = 0;
+    best_perm<0>(rm, cbest, qbest);
+    if (cbest < best) {
+      best = cbest;
+      const uint32_t pr = kPerms[qbest];
+      uint32_t rho = 0;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const uint32_t a = (code >> (8 * i)) & 0xF, b = (code >> (8 * i + 4)) & 0xF;
-          const uint32_t ri = (pr >> (2 * i)) & 3;
-          rho |= (ri << (2 * a)) | (ri << (2 * b));
-        }
-        best_rho = rho;
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t a = (code >> (8 * i)) & 0xF, b = (code >> (8 * i + 4)) & 0xF;
+        const uint32_t ri = (pr >> (2 * i)) & 3;
+        rho |= (ri << (2 * a)) | (ri << (2 * b));
       }
+      best_rho = rho;
     }
   }
   return best_rho;
