@@ -741,20 +741,36 @@ __global__ void __launch_bounds__(256) finish_vec4_kernel(
     }
     if (sg != 0 || v >= total4) continue;
     const int64_t t = v * 4, i = t / b, c = t - i * b;
-    if (tail) {
-      const uint32_t tc = tailp[i];
-      for (int u = 0; u < tail; ++u) {
-        const float w = vals.v[(tc >> (4 * u)) & 0xF];
-        const int64_t xo = (nb * d + u) * b + c;
-        a.x = fmaf(w, load_as<float>(x, x_dtype, xo), a.x);
-        a.y = fmaf(w, load_as<float>(x, x_dtype, xo + 1), a.y);
-        a.z = fmaf(w, load_as<float>(x, x_dtype, xo + 2), a.z);
-        a.w = fmaf(w, load_as<float>(x, x_dtype, xo + 3), a.w);
+    if (b % 4 == 0) {  // the four outputs share row i
+      if (tail) {
+        const uint32_t tc = tailp[i];
+        for (int u = 0; u < tail; ++u) {
+          const float w = vals.v[(tc >> (4 * u)) & 0xF];
+          const int64_t xo = (nb * d + u) * b + c;
+          a.x = fmaf(w, load_as<float>(x, x_dtype, xo), a.x);
+          a.y = fmaf(w, load_as<float>(x, x_dtype, xo + 1), a.y);
+          a.z = fmaf(w, load_as<float>(x, x_dtype, xo + 2), a.z);
+          a.w = fmaf(w, load_as<float>(x, x_dtype, xo + 3), a.w);
+        }
       }
-    }
-    if (scale_mode == MSG_SCALE_PER_ROW) {
-      const float qs = load_as<float>(q, q_dtype, i);
-      a.x *= qs; a.y *= qs; a.z *= qs; a.w *= qs;
+      if (scale_mode == MSG_SCALE_PER_ROW) {
+        const float qs = load_as<float>(q, q_dtype, i);
+        a.x *= qs; a.y *= qs; a.z *= qs; a.w *= qs;
+      }
+    } else {           // b % 4 != 0 (m b % 4 == 0): the four outputs may span rows
+      float* av[4] = {&a.x, &a.y, &a.z, &a.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int64_t ie = (t + e) / b, ce = (t + e) - ie * b;
+        float r = *av[e];
+        if (tail) {
+          const uint32_t tc = tailp[ie];
+          for (int u = 0; u < tail; ++u)
+            r = fmaf(vals.v[(tc >> (4 * u)) & 0xF], load_as<float>(x, x_dtype, (nb * d + u) * b + ce), r);
+        }
+        if (scale_mode == MSG_SCALE_PER_ROW) r *= load_as<float>(q, q_dtype, ie);
+        *av[e] = r;
+      }
     }
     if (y_dtype == MSG_F16) {
       __half2 h0 = __floats2half2_rn(a.x, a.y), h1 = __floats2half2_rn(a.z, a.w);
@@ -1096,7 +1112,9 @@ int launch_finish(const float* partial, int S, int64_t m, int64_t b, int64_t k, 
   // four outputs per thread group; slices split over SG groups when there are
   // few outputs per SM (e.g. 137 slices x 8192 x 4)
   // (float4 / uint2 stores of Y: a caller-supplied Y must be 16-byte aligned)
-  if (b % 4 == 0 && scale_mode != MSG_SCALE_PER_GROUP && S >= 2 &&
+  // (b % 4 != 0 is fine as long as m b % 4 == 0: the flat output index is
+  // vectorised and every element finds its own row)
+  if (total % 4 == 0 && scale_mode != MSG_SCALE_PER_GROUP && S >= 2 &&
       (reinterpret_cast<uintptr_t>(y) & 15) == 0) {
     int sg = 1;
     while (sg < 16 && 2 * sg <= S && (total / 4) * sg < (int64_t)sm_count() * 512) sg *= 2;

@@ -533,6 +533,28 @@ __device__ __forceinline__ void slice_correction(const RbParams& P, int r_begin,
   __syncthreads();
 }
 
+// one row's partials of a column tile: the widest aligned stores the tile
+// allows (float4 when the row stride b and the valid columns are multiples of
+// 4, float2 for multiples of 2; a partly filled last tile of b = 6, 12, ...
+// otherwise fell back to strided scalar stores, measured 25 % slower kernels)
+template <int BC>
+__device__ __forceinline__ void store_partial_row(float* dst, const float* v, int64_t b, int64_t c0) {
+  const int64_t nvc = b - c0 < BC ? b - c0 : BC;   // valid columns of this tile
+  if ((b & 3) == 0 && (nvc & 3) == 0) {
+#pragma unroll
+    for (int c = 0; c < BC; c += 4)
+      if (c < nvc) *reinterpret_cast<float4*>(dst + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+  } else if ((b & 1) == 0 && (nvc & 1) == 0) {
+#pragma unroll
+    for (int c = 0; c < BC; c += 2)
+      if (c < nvc) *reinterpret_cast<float2*>(dst + c) = make_float2(v[c], v[c + 1]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < BC; ++c)
+      if (c < nvc) dst[c] = v[c];
+  }
+}
+
 // (a & b) | (c & ~b): the table slot bits come from c, the entry bits from a
 __device__ __forceinline__ uint32_t lop3_mux(uint32_t a, uint32_t mask, uint32_t c) {
   uint32_t r;
@@ -789,15 +811,7 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_lut_kernel(RbParams P) {
     float v[BC];
 #pragma unroll
     for (int c = 0; c < BC; ++c) v[c] = acc[r][c] + cv[c];
-    if (c0 + BC <= P.b && (P.b % 4) == 0 && BC >= 4) {
-#pragma unroll
-      for (int c = 0; c < BC; c += 4)
-        *reinterpret_cast<float4*>(dst + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
-    } else {
-#pragma unroll
-      for (int c = 0; c < BC; ++c)
-        if (c0 + c < P.b) dst[c] = v[c];
-    }
+    store_partial_row<BC>(dst, v, P.b, c0);
   }
 }
 
@@ -1035,16 +1049,10 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_tmem_kernel(RbParams P) {
       const int r = 2 * p + h;
       if (r >= nvalid) continue;
       float* dst = P.partial + ((int64_t)slice * P.m + my_row + r) * P.b + c0;
-      if (c0 + BC <= P.b && (P.b % 4) == 0) {
-        *reinterpret_cast<float4*>(dst) = make_float4(v[8 * h] + cv[0], v[8 * h + 1] + cv[1],
-                                                      v[8 * h + 2] + cv[2], v[8 * h + 3] + cv[3]);
-        *reinterpret_cast<float4*>(dst + 4) = make_float4(v[8 * h + 4] + cv[4], v[8 * h + 5] + cv[5],
-                                                          v[8 * h + 6] + cv[6], v[8 * h + 7] + cv[7]);
-      } else {
+      float vr[BC];
 #pragma unroll
-        for (int c = 0; c < BC; ++c)
-          if (c0 + c < P.b) dst[c] = v[8 * h + c] + cv[c];
-      }
+      for (int c = 0; c < BC; ++c) vr[c] = v[8 * h + c] + cv[c];
+      store_partial_row<BC>(dst, vr, P.b, c0);
     }
   }
   tm_fence_before();
@@ -1057,7 +1065,11 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_tmem_kernel(RbParams P) {
 // ============================================================================
 // host side
 // ============================================================================
-int rb_group_count(int64_t b) { return b >= 8 ? 4 : (b >= 4 ? 8 : 16); }
+// tables per round from the batch: 8-column tiles (rounds of 4 groups) from
+// b = 5 -- one padded tile beats 4 + (b - 4) columns in two tiles (b = 6 at
+// cfg4: 48 + 15 -> ~39 + 8 us) -- 4-column tiles for b = 2..4 (measured b = 2
+// on 4-column tiles slower than on the 2-column kernel, so that stays)
+int rb_group_count(int64_t b) { return b >= 5 ? 4 : (b >= 4 ? 8 : 16); }
 
 bool rb_eligible(int width, int x_dtype, int64_t b, int d, int scale_mode, bool sym,
                  bool f32_entries, bool s_exact16) {

@@ -66,7 +66,7 @@ def test_plan_configs_take_fused_symmetric_path(m, k, b, d):
     assert st == 0 and lay == _lib.LAYOUT_QUAD
 
 
-@pytest.mark.parametrize("b,want", [(2, 6), (3, 6), (4, 5), (7, 5), (8, 7), (16, 7), (64, 4)])
+@pytest.mark.parametrize("b,want", [(2, 6), (3, 6), (4, 5), (5, 7), (7, 7), (8, 7), (16, 7), (64, 4)])
 def test_plan_rowblock_round_width(b, want):
     st, lay, sym, ws = _plan(8192, 8192, b, 3)
     assert st == 0 and lay == want
