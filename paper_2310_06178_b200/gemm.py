@@ -143,6 +143,10 @@ def msgemm(pwm: PackedWeightMatrix, X, d: int, budget: int = DEFAULT_BUDGET,
     # reusing its pinned buffers): validation and plan lookup were done on
     # the first call; only the buffers' identity, shape and stream are checked
     fast = getattr(pwm, "_device_cache", None)
+    if fast is None and id(pwm) in _FOREIGN:           # a wrapped reference-typed object
+        fent = _FOREIGN[id(pwm)]
+        if fent[0]() is pwm:
+            fast = fent[1]._device_cache
     if fast is not None:
         ent = fast.get(("fast", id(X), id(out), d, budget, table_dtype, symmetric, out_dtype, _flags))
         if ent is not None:
