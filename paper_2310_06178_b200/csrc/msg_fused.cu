@@ -1112,10 +1112,12 @@ int launch_finish(const float* partial, int S, int64_t m, int64_t b, int64_t k, 
   // four outputs per thread group; slices split over SG groups when there are
   // few outputs per SM (e.g. 137 slices x 8192 x 4)
   // (float4 / uint2 stores of Y: a caller-supplied Y must be 16-byte aligned)
-  // (b % 4 != 0 is fine as long as m b % 4 == 0: the flat output index is
-  // vectorised and every element finds its own row)
-  if (total % 4 == 0 && scale_mode != MSG_SCALE_PER_GROUP && S >= 2 &&
-      (reinterpret_cast<uintptr_t>(y) & 15) == 0) {
+  // (b % 4 != 0 works as long as m b % 4 == 0: the flat output index is
+  // vectorised and every element finds its own row -- worth it with enough
+  // outputs to fill the GPU: for a GEMV-sized m b the scalar kernel keeps
+  // four times more threads busy)
+  if (total % 4 == 0 && (b % 4 == 0 || total >= 32768) && scale_mode != MSG_SCALE_PER_GROUP &&
+      S >= 2 && (reinterpret_cast<uintptr_t>(y) & 15) == 0) {
     int sg = 1;
     while (sg < 16 && 2 * sg <= S && (total / 4) * sg < (int64_t)sm_count() * 512) sg *= 2;
     const int opb = 256 / sg;
