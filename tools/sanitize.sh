@@ -13,3 +13,9 @@ for tool in memcheck racecheck synccheck initcheck; do
       python tools/sanitize_probe.py > $O/$tool.log 2>&1
   echo "$tool rc=$?: $(tail -1 $O/$tool.log)"
 done
+
+# compute-sanitizer is closed on this pool: the stand-in is the whole GPU suite
+# on the debug-checks library (in-kernel bounds asserts + barrier jitter)
+MSG_LIB_VARIANT=debug python -m pytest tests -m gpu -q --deselect tests/test_gpu_debug_build.py \
+    > $O/pytest_gpu_debug_library.log 2>&1
+echo "debug-library suite rc=$?: $(tail -1 $O/pytest_gpu_debug_library.log)"
