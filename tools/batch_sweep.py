@@ -47,7 +47,7 @@ def timed(fn):
 
 
 print(f"{'b':>4s} {'msGeMM us':>10s} {'dense us':>9s} {'ratio':>6s}")
-for b in (1, 2, 3, 4, 6, 8, 12, 16, 32):
+for b in [int(v) for v in __import__("os").environ.get("BS", "1,2,3,4,6,8,12,16,32").split(",")]:
     x = torch.from_numpy(rng.standard_normal((k, b)).astype(np.float16)).cuda()
     Y = torch.empty((m, b), dtype=torch.float16, device="cuda")
     Yd = torch.empty((m, b), dtype=torch.float32, device="cuda")
