@@ -102,38 +102,42 @@ __global__ void __launch_bounds__(256) repack_lane_kernel(const uint8_t* __restr
     const int lane = tid & 31, cc = tid >> 5;
     const int64_t c = c0 + cc, i = i0 + lane;
     if (c >= L.nchunk) continue;
-    uint32_t w[16] = {0};
-    if (i < m) {
+    // field of position p (16 bits): the group's 11-bit folded index as the
+    // table address >> 1 plus the sign bit
+    auto field = [&](int p) -> uint32_t {
+      const int gl = p ^ lane;                         // group of position p inside the chunk
+      const int64_t j = c * 32 + gl;
+      if (i >= m || j >= L.nb) return 0;
+      uint32_t idx = 0;
 #pragma unroll
-      for (int p = 0; p < 32; ++p) {
-        const int gl = p ^ lane;                       // group of position p inside the chunk
-        const int64_t j = c * 32 + gl;
-        uint32_t f = 0, sign = 0;
-        if (j < L.nb) {
-          uint32_t idx = 0;
-#pragma unroll
-          for (int c3 = 0; c3 < 3; ++c3) {
-            const int cd = cc * 96 + 3 * gl + c3;      // code inside the tile row
-            idx |= ((tile[lane][cd >> 1] >> ((cd & 1) * 4)) & 0xF) << (4 * c3);
-          }
-          if (idx & 0x800) { idx ^= 0xFFF; sign = 1; }  // sign symmetry: complement
-          f = idx;                                       // 11 bits
-        }
-        const uint32_t F = ((f & 0x3FF) << 6) | (sign << 1) | (f >> 10);
-        w[p >> 1] |= F << (16 * (p & 1));
+      for (int c3 = 0; c3 < 3; ++c3) {
+        const int cd = cc * 96 + 3 * gl + c3;          // code inside the tile row
+        idx |= ((tile[lane][cd >> 1] >> ((cd & 1) * 4)) & 0xF) << (4 * c3);
       }
-      if (L.tail && c == 0) {
-        const uint8_t* row = packed + i * rb;
-        uint32_t tc = 0;
-        for (int64_t jj = L.nb * 3; jj < k; ++jj)
-          tc |= ((row[jj >> 1] >> ((jj & 1) * 4)) & 0xF) << (4 * (jj - L.nb * 3));
-        reinterpret_cast<uint16_t*>(out + L.tail_off)[i] = (uint16_t)tc;
-      }
-    }
+      uint32_t sign = 0;
+      if (idx & 0x800) { idx ^= 0xFFF; sign = 1; }    // sign symmetry: complement
+      return ((idx & 0x3FF) << 6) | (sign << 1) | (idx >> 10);
+    };
+    // one 16-byte record (8 positions) at a time: few live registers, so the
+    // repack runs at full occupancy
     uint4* base = reinterpret_cast<uint4*>(out + L.body_off) + (c * L.ntiles + tl) * 128;
+#pragma unroll 1
+    for (int v = 0; v < 4; ++v) {
+      uint32_t w4[4];
 #pragma unroll
-    for (int v = 0; v < 4; ++v)
-      base[v * 32 + lane] = make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
+      for (int e = 0; e < 4; ++e) {
+        const int p = 8 * v + 2 * e;
+        w4[e] = field(p) | (field(p + 1) << 16);
+      }
+      base[v * 32 + lane] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+    }
+    if (i < m && L.tail && c == 0) {
+      const uint8_t* row = packed + i * rb;
+      uint32_t tc = 0;
+      for (int64_t jj = L.nb * 3; jj < k; ++jj)
+        tc |= ((row[jj >> 1] >> ((jj & 1) * 4)) & 0xF) << (4 * (jj - L.nb * 3));
+      reinterpret_cast<uint16_t*>(out + L.tail_off)[i] = (uint16_t)tc;
+    }
   }
 }
 

@@ -121,18 +121,20 @@ __global__ void __launch_bounds__(256) repack_rb_kernel(const uint8_t* __restric
       const int r = e % kRpTileRows, qq = e / kRpTileRows;
       const int64_t i = i0 + r, q = q0 + qq;
       if (i >= L.mp || q >= L.nqp) continue;
-      const int qr = G / 4;
-      const int64_t round = q / qr;
-      const int qin = (int)(q % qr);
+      // G, rows per thread and rows per CTA are powers of two: shifts and masks
+      const int lg = G == 8 ? 3 : 4;                   // log2 G (G = 8 or 16 here)
+      const int lrpt = G == 8 ? 3 : 2;                 // log2 rb_rows_per_thread(G)
+      const int64_t round = q >> (lg - 2);
+      const int qin = (int)(q & ((G >> 2) - 1));
+      // lanes own rows: thread tid of a CTA holds rows tid * RPT .. + RPT - 1 of
+      // its row block, and its position p looks up group (p + tid) mod G
+      const int lane = (int)((i & ((int64_t)kRbThreads << lrpt) - 1) >> lrpt);
       uint32_t f[4] = {0, 0, 0, 0}, sg[4] = {0, 0, 0, 0};
       if (i < m) {
+#pragma unroll
         for (int s = 0; s < 4; ++s) {
           const int p = 4 * qin + s;
-          // lanes own rows: thread tid of a CTA holds rows tid * RPT .. + RPT - 1 of
-          // its row block, and its position p looks up group (p + tid) mod G
-          const int rpt = rb_rows_per_thread(G);
-          const int64_t lane = (i % (kRbThreads * rpt)) / rpt;
-          const int g = (int)((p + lane) % G);         // group of this position in the round
+          const int g = (p + lane) & (G - 1);          // group of this position in the round
           const int64_t j = round * G + g;             // global group
           if (j >= L.nb) continue;
           const int lq = (int)(j / 4 - q0);            // its quad inside this tile
