@@ -200,8 +200,8 @@ constexpr int kRb4Cands = 4;  // pairings searched (simulated: top-4 matches top
 // rotations (2 bits per lane) of one octet from the lanes' 4-bit parity masks
 // pmw (lane u at bits 4u..4u+3).  The kRb4Cands pairings with the fewest
 // equal-parity (pair, table) incidences are searched over the 24 rotation
-// permutations (ties: earlier pairings first); cand/cscore are this thread's
-// slots in shared memory (dynamically indexed, so not in registers).
+// permutations (ties: earlier pairings first).
+//
 // the 4 lane pairs of every pairing as indices into the 28 pairs (a < b),
 // pair (a, b) -> a (15 - a) / 2 + b - a - 1 (compile-time copy of kPairings)
 __host__ __device__ constexpr int pair_idx(int p, int i) {
@@ -231,25 +231,26 @@ __host__ __device__ constexpr uint32_t perm_code(int q) {
   return t[q];
 }
 
-// pairing P's score (equal-parity incidences) into the running top-K; template
+// pairing P's score (equal-parity incidences) into the running top 4, kept
+// in registers sorted by score (ties: earlier pairings first) with predicated
+// compare-and-swaps -- no shared memory, no divergent insertion loop; template
 // recursion so every pair index is a compile-time constant (pc stays in registers)
+struct Top4 { int s0, s1, s2, s3, c0, c1, c2, c3; };
 template <int P>
-__device__ __forceinline__ void score_pairings(const int (&pc)[28], int& nc, int& worst, uint8_t* cand,
-                                               uint8_t* cscore) {
+__device__ __forceinline__ void score_pairings(const int (&pc)[28], Top4& t) {
   if constexpr (P < 105) {
     const int sc = pc[pair_idx(P, 0)] + pc[pair_idx(P, 1)] + pc[pair_idx(P, 2)] + pc[pair_idx(P, 3)];
-    if (nc < kRb4Cands || sc < worst) {  // keep the best (stable: earlier first)
-      int pos = nc < kRb4Cands ? nc++ : kRb4Cands - 1;
-      while (pos > 0 && cscore[pos - 1] > sc) {
-        cand[pos] = cand[pos - 1];
-        cscore[pos] = cscore[pos - 1];
-        --pos;
+    if (sc < t.s3) {
+      t.s3 = sc; t.c3 = P;
+      if (t.s3 < t.s2) {
+        int x = t.s2; t.s2 = t.s3; t.s3 = x; x = t.c2; t.c2 = t.c3; t.c3 = x;
+        if (t.s2 < t.s1) {
+          x = t.s1; t.s1 = t.s2; t.s2 = x; x = t.c1; t.c1 = t.c2; t.c2 = x;
+          if (t.s1 < t.s0) { x = t.s0; t.s0 = t.s1; t.s1 = x; x = t.c0; t.c0 = t.c1; t.c1 = x; }
+        }
       }
-      cand[pos] = (uint8_t)P;
-      cscore[pos] = (uint8_t)sc;
-      worst = nc < kRb4Cands ? 99 : cscore[kRb4Cands - 1];
     }
-    score_pairings<P + 1>(pc, nc, worst, cand, cscore);
+    score_pairings<P + 1>(pc, t);
   }
 }
 
@@ -265,18 +266,21 @@ __device__ __forceinline__ void best_perm(const uint32_t (&rm)[4], int& cbest, i
   }
 }
 
-__device__ uint32_t choose_rotations(uint32_t pmw, uint8_t* cand, uint8_t* cscore) {
+__device__ uint32_t choose_rotations(uint32_t pmw) {
   // equal-parity count of every lane pair, once (the 105 pairings reuse them)
   int pc[28];
 #pragma unroll
   for (int a = 0, n = 0; a < 8; ++a)
 #pragma unroll
     for (int b = a + 1; b < 8; ++b, ++n) pc[n] = __popc(~((pmw >> (4 * a)) ^ (pmw >> (4 * b))) & 0xF);
-  int nc = 0, worst = 99;
-  score_pairings<0>(pc, nc, worst, cand, cscore);
+  static_assert(kRb4Cands == 4, "the register top-K keeps 4 candidates");
+  Top4 t{99, 99, 99, 99, 0, 0, 0, 0};
+  score_pairings<0>(pc, t);
+  const int cand[4] = {t.c0, t.c1, t.c2, t.c3};
   int best = 99;
   uint32_t best_rho = 0;
-  for (int c = 0; c < nc; ++c) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
     const uint32_t code = kPairings[cand[c]];
     uint32_t rm[4];  // the pair's bad-position mask under rotation r at bits 4r..4r+3
 #pragma unroll
@@ -319,7 +323,6 @@ __global__ void __launch_bounds__(128) repack_rb4_kernel(const uint8_t* __restri
   constexpr int NGRP = kRb4Rows / RPT;              // RPT-row groups per 128 rows
   __shared__ uint8_t tile[kRb4Rows][kRb4Quads * 6 + 4];
   __shared__ uint16_t rho_s[kRb4Quads][NSUB][RPT];
-  __shared__ uint8_t cand_s[128][kRb4Cands], csc_s[128][kRb4Cands];
   const int tid = threadIdx.x;
   uint32_t* lo_p = reinterpret_cast<uint32_t*>(out + L.lo_off);
   uint16_t* hi_p = reinterpret_cast<uint16_t*>(out + L.hi_off);
@@ -372,7 +375,7 @@ __global__ void __launch_bounds__(128) repack_rb4_kernel(const uint8_t* __restri
           uint32_t sg;
           pmw |= (rec(tr0 + RPT * u, g, sg) & 1) << (4 * u + g);
         }
-      const uint32_t rho = choose_rotations(pmw, cand_s[tid], csc_s[tid]);
+      const uint32_t rho = choose_rotations(pmw);
       rho_s[qq][sub][r] = (uint16_t)rho;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
