@@ -367,14 +367,23 @@ __global__ void __launch_bounds__(128) repack_rb4_kernel(const uint8_t* __restri
         return idx;
       };
       const int tr0 = 8 * RPT * sub + r;               // tile row of lane u = 0
+      // each lane's 4 records (11-bit folded index | sign << 11) at bits 12 g,
+      // extracted once and reused for the rotated writes (64-bit shifts, no
+      // dynamically indexed arrays)
+      uint64_t recs[8];
       uint32_t pmw = 0;
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+      for (int u = 0; u < 8; ++u) {
+        uint64_t rw = 0;
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           uint32_t sg;
-          pmw |= (rec(tr0 + RPT * u, g, sg) & 1) << (4 * u + g);
+          const uint32_t f = rec(tr0 + RPT * u, g, sg);
+          pmw |= (f & 1) << (4 * u + g);
+          rw |= (uint64_t)(f | (sg << 11)) << (12 * g);
         }
+        recs[u] = rw;
+      }
       const uint32_t rho = choose_rotations(pmw);
       rho_s[qq][sub][r] = (uint16_t)rho;
 #pragma unroll
@@ -383,9 +392,16 @@ __global__ void __launch_bounds__(128) repack_rb4_kernel(const uint8_t* __restri
         const int64_t i = base + tr;
         if (i >= L.mp) continue;
         const uint32_t ru = (rho >> (2 * u)) & 3;
+        // position s2 holds group (s2 + ru) mod 4: rotate the 48-bit record set
+        const uint64_t rw = recs[u];
+        const uint64_t rot = ((rw >> (12 * ru)) | (rw << (48 - 12 * ru))) & 0xFFFFFFFFFFFFull;
         uint32_t ff[4], ss[4];
 #pragma unroll
-        for (int s2 = 0; s2 < 4; ++s2) ff[s2] = rec(tr, (s2 + ru) & 3, ss[s2]);
+        for (int s2 = 0; s2 < 4; ++s2) {
+          const uint32_t v = (uint32_t)(rot >> (12 * s2)) & 0xFFF;
+          ff[s2] = v & 0x7FF;
+          ss[s2] = v >> 11;
+        }
         lo_p[q * L.mp + i] = ff[0] | (ff[1] << 11) | ((ff[2] & 0x3FF) << 22);
         hi_p[q * L.mp + i] = (uint16_t)((ff[2] >> 10) | (ff[3] << 1) | (ss[0] << 12) |
                                         (ss[1] << 13) | (ss[2] << 14) | (ss[3] << 15));
