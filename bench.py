@@ -306,7 +306,7 @@ def main():
             dist.all_reduce(Yshard, op=dist.ReduceOp.SUM)   # Yshard: this rank's fp32 partial
         else:
             dist.all_gather_into_tensor(Yfull, Yshard)
-    TC = -1  # pseudo-flag: the dequant + tcgen05.mma comparison kernel (K4) instead of msGeMM
+    TC = -1  # pseudo-flag: the dense dequantise-then-multiply comparison kernel (K4) instead of msGeMM
     xd16 = xd.half()
     Ytc = torch.empty((mr, cfg.b), dtype=torch.float32, device=dev)
 
@@ -523,7 +523,9 @@ def main():
                         ("H2D X slice, msgemm k-slice, NCCL all-reduce, D2H Y" if ksplit else
                          "H2D X, msgemm shard, NCCL all-gather, D2H Y")},
         "tensor_core_baseline": None if ms_tc is None else {
-            "kernel": "K4: int4->fp16 dequant + tcgen05.mma kind::f16, fp32 TMEM accumulation",
+            "kernel": ("K4: weight-streaming int4->fp16 dequant + mma.sync m16n8k16, fp32 accumulation, "
+                       "cluster split-k over DSMEM" if shard_cfg.b <= 16 and shard_cfg.k % 32 == 0 else
+                       "K4: int4->fp16 dequant + tcgen05.mma kind::f16, fp32 TMEM accumulation"),
             "ms_per_step": ms_tc, "value": effective_ops(shard_cfg) / (ms_tc * 1e-3) / 1e9,
             "unit": "GOP/s (this rank's shard, no all-gather)",
             "hbm_frac": algorithmic_bytes(shard_cfg, 2, 4) / (ms_tc * 1e-3) / 1e9 / peaks["hbm_gbs"]},

@@ -198,6 +198,15 @@ MSG_API int msg_dequant_gemv(const uint8_t* packed, int64_t m, int64_t k, const 
                              const void* x, int x_dtype, int64_t b, void* y, int y_dtype,
                              void* stream);
 
+/* Dense comparison baseline for 1 <= b <= 16, same inputs and result contract
+ * as msg_dequant_gemv: the packed rows are streamed once, dequantised in
+ * registers and multiplied with mma.sync m16n8k16 (fp32 accumulation); split
+ * k across a thread-block cluster, partial tiles summed through distributed
+ * shared memory in rank order (one kernel, no workspace, deterministic). */
+MSG_API int msg_dequant_hmma(const uint8_t* packed, int64_t m, int64_t k, const double* values,
+                             const void* x, int x_dtype, int64_t b, void* y, int y_dtype,
+                             void* stream);
+
 /* ---------- dense reference product (gemm.py:206-216 naive_gemm) ---------- */
 /* Y (m,b) = W (m,k) @ X (k,b), operands of any supported dtype, converted
  * in-kernel.  mode 0: both integer -> int64 Y, wrapping int64 arithmetic

@@ -602,22 +602,26 @@ def naive_gemm_counted(W, X):
     return Y, OpCount(fma=m * k * b, mem_weights=m * k, mem_activations=k * b)
 
 
-_GEMV_MAX_B = 1   # dense baseline: CUDA-core GEMV at b = 1, tcgen05 above (measured: tie at b = 2)
+_HMMA_MAX_B = 16   # dense baseline: weight-streaming mma.sync kernel up to b = 16, tcgen05 above
 
 
 def dequant_gemm(pwm: PackedWeightMatrix, X, out_dtype=np.float32, out=None, kernel="auto"):
     """Dense comparison baseline (K4): dequantise int4 W and multiply, fp32
-    accumulation -- on the CUDA cores straight from the packed layout for
-    small batches (csrc/msg_dense.cu, weight-stream bound), else on the
-    tcgen05 tensor cores (csrc/msg_mma.cu, accumulator in TMEM).
+    accumulation -- for b <= 16 a weight-streaming kernel straight from the
+    packed layout (csrc/msg_dense_hmma.cu: in-register dequantise + mma.sync,
+    split k over a thread-block cluster), else on the tcgen05 tensor cores
+    (csrc/msg_mma.cu, accumulator in TMEM).
 
     X must be fp16 (k,) or (k, b) with b <= 256; int4/uint4 codebooks, no
     scales.  Same result contract as naive_gemm(dense(pwm), X) (gemm.py:206-216).
-    kernel: "auto" | "gemv" (b <= 8, k % 32 == 0) | "mma".
+    kernel: "auto" | "hmma" (b <= 16, k % 32 == 0) | "gemv" (the CUDA-core
+    variant, b <= 8, k % 32 == 0) | "mma".
     """
     pwm = _ensure_device_pwm(pwm)
     if pwm.scales is not None:
         raise NotImplementedError("dequant_gemm does not apply scales")
+    if kernel not in ("auto", "hmma", "gemv", "mma"):
+        raise ValueError(f"unknown dense kernel {kernel!r}")
     Xm, was_vector = _as_matrix(X)
     if int(Xm.shape[0]) != pwm.k:
         raise ValueError(f"activation rows {Xm.shape[0]} != weight columns {pwm.k}")
@@ -630,12 +634,16 @@ def dequant_gemm(pwm: PackedWeightMatrix, X, out_dtype=np.float32, out=None, ker
     Y = out if out is not None else t.empty((m, b), dtype=y_dt, device=dev)
     cbv = [float(v) for v in pwm.codebook.values]
     nib = cbv == [float(c if c < 8 else c - 16) for c in range(16)] or cbv == [float(c) for c in range(16)]
-    gemv_ok = b <= 8 and k % 32 == 0 and nib and xd.dtype == t.float16
-    use_gemv = gemv_ok and (kernel == "gemv" or (kernel == "auto" and b <= _GEMV_MAX_B))
-    if kernel == "gemv" and not gemv_ok:
+    stream_ok = k % 32 == 0 and nib and xd.dtype == t.float16
+    if kernel == "gemv" and not (stream_ok and b <= 8):
         raise NotImplementedError("the GEMV baseline needs b <= 8, k % 32 == 0, int4/uint4 and fp16 X")
-    if m and b and use_gemv:
-        _lib.check(lib.msg_dequant_gemv(
+    if kernel == "hmma" and not (stream_ok and b <= _HMMA_MAX_B):
+        raise NotImplementedError("the HMMA baseline needs b <= 16, k % 32 == 0, int4/uint4 and fp16 X")
+    if kernel == "auto":
+        kernel = "hmma" if stream_ok and b <= _HMMA_MAX_B else "mma"
+    if m and b and kernel in ("hmma", "gemv"):
+        fn = lib.msg_dequant_hmma if kernel == "hmma" else lib.msg_dequant_gemv
+        _lib.check(fn(
             _lib.ptr(pwm.device_data(dev)), m, k, _lib.host_doubles(pwm.codebook.values),
             _lib.ptr(xd.contiguous()), _lib.dtype_code(xd.dtype), b, _lib.ptr(Y),
             _lib.dtype_code(y_dt), _lib.stream_ptr()))

@@ -1,8 +1,8 @@
-"""The dense comparison baseline (K4) on both of its kernels -- the CUDA-core
-GEMV for small batches (csrc/msg_dense.cu) and the tcgen05 kernel
-(csrc/msg_mma.cu) -- against the oracle's naive_gemm(dense(pwm), X)
+"""The dense comparison baseline (K4) on its three kernels -- the
+weight-streaming mma.sync kernel for b <= 16 (csrc/msg_dense_hmma.cu), the
+CUDA-core GEMV (csrc/msg_dense.cu) and the tcgen05 kernel (csrc/msg_mma.cu) -- against the oracle's naive_gemm(dense(pwm), X)
 (gemm.py:206-216).  Integer-valued X: every product and partial sum is an
-integer below 2^24, so both kernels must be bit-exact; fp16 X: the
+integer below 2^24, so every kernel must be bit-exact; fp16 X: the
 reference's rule with rtol 2e-3 (suites.py:104-124)."""
 
 import numpy as np
@@ -14,7 +14,7 @@ from oracle import msgemm_oracle as orc
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("kernel", ["gemv", "mma"])
+@pytest.mark.parametrize("kernel", ["hmma", "gemv", "mma"])
 @pytest.mark.parametrize("m,k,b", [(1, 32, 1), (37, 96, 2), (300, 1056, 3), (129, 4096, 4),
                                    (1000, 2048, 8), (64, 8192, 1), (8192, 1024, 5)])
 @pytest.mark.parametrize("cb", ["int4", "uint4"])
@@ -48,3 +48,29 @@ def test_dense_baseline_vector_and_auto_dispatch():
     with pytest.raises(NotImplementedError):
         mg.dequant_gemm(mg.from_codes(codes[:, :100], mg.int4_codebook()),
                         torch.from_numpy(x[:100]).cuda(), kernel="gemv")      # k % 32 != 0
+
+
+@pytest.mark.parametrize("m,k,b", [(130, 128, 9), (777, 4096, 16), (1, 8192, 13), (4096, 4096, 1),
+                                   (2049, 2080, 11), (256, 32, 16), (8192, 8192, 8)])
+@pytest.mark.parametrize("split", [None, "1", "2", "8"])
+def test_dense_hmma_wide_batches_and_splits(m, k, b, split, monkeypatch):
+    """b = 9..16 (second n-tile), every cluster size of the k split, ragged
+    rows and k tails -- bit-exact against numpy for integer X, repeatable."""
+    import torch
+    if split is None:
+        monkeypatch.delenv("MSG_DH_SPLIT", raising=False)
+    else:
+        monkeypatch.setenv("MSG_DH_SPLIT", split)
+    rng = np.random.default_rng(m * 7 + k + b)
+    codes = rng.integers(0, 16, (m, k), dtype=np.uint8)
+    pwm = mg.from_codes(codes, mg.int4_codebook())
+    W = orc.int4_values()[codes]
+    Xi = rng.integers(-30, 31, (k, b))
+    xd = torch.from_numpy(Xi.astype(np.float16)).cuda()
+    y1 = mg.dequant_gemm(pwm, xd, kernel="hmma")
+    y2 = mg.dequant_gemm(pwm, xd, kernel="hmma")
+    assert torch.equal(y1, y2)
+    assert np.array_equal(y1.cpu().numpy().astype(np.int64), W.astype(np.int64) @ Xi.astype(np.int64))
+    X = rng.standard_normal((k, b)).astype(np.float16)
+    y = mg.dequant_gemm(pwm, torch.from_numpy(X).cuda(), kernel="hmma").cpu().numpy()
+    assert orc.rel_error(y, W, X) <= 2e-3

@@ -49,6 +49,10 @@ def main():
     ks = [mg.dequant_gemm(pwm, Xh).cpu().numpy() for _ in range(reps)]
     assert all(k.tobytes() == ks[0].tobytes() for k in ks), "dq_mma not repeatable"
     res["k4"] = ks[0]
+    for nb in (1, 8, 13):                                   # dq_hmma: cluster split-k over DSMEM
+        hs = [mg.dequant_gemm(pwm, Xh[:, :nb].contiguous(), kernel="hmma").cpu().numpy() for _ in range(reps)]
+        assert all(h.tobytes() == hs[0].tobytes() for h in hs), "dq_hmma not repeatable"
+        res[f"k4h{nb}"] = hs[0]
     torch.cuda.synchronize()
     np.savez(out, lib=np.frombuffer(str(_lib.LIB_PATH.name).encode(), dtype=np.uint8), **res)
     print(f"debug probe ok ({_lib.LIB_PATH.name}, {len(CASES)} cases x {reps})")

@@ -35,7 +35,7 @@ def main():
         rf, tc = d["roofline"], d.get("tensor_core_baseline") or {}
         print(f"{c:9s} msGeMM {d['value']:10.1f} GOP/s  step {d['ms_per_step']*1e3:8.1f} us  "
               f"LUT kernel {rf['kernel_ms']*1e3:8.1f} us  HBM {rf['frac']*100:5.1f}%  "
-              f"| K4 tensor-core {tc.get('value', float('nan')):10.1f} GOP/s "
+              f"| K4 dense {tc.get('value', float('nan')):10.1f} GOP/s "
               f"({tc.get('ms_per_step', float('nan'))*1e3:7.1f} us, HBM {tc.get('hbm_frac', float('nan'))*100:5.1f}%)",
               flush=True)
     Path(a.out).parent.mkdir(parents=True, exist_ok=True)
