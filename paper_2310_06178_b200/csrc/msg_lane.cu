@@ -260,8 +260,11 @@ __device__ __forceinline__ FinishPair finish_prefetch(const LaneParams& P, int64
 }
 // the tail is added to the rounded fp32 sum, as the reference adds it to the
 // block sum (gemm.py:81-83); the sums are read through L2 and cleared
-__device__ __forceinline__ void finish_pair(const LaneParams& P, int64_t row, const FinishPair& f) {
-  if (row >= P.m) return;
+// values of rows (row, row + 1); false when row >= m
+__device__ __forceinline__ bool finish_pair_values(const LaneParams& P, int64_t row, const FinishPair& f,
+                                                   float& y0, float& y1) {
+  y0 = y1 = 0.f;
+  if (row >= P.m) return false;
   ulonglong2* ap = reinterpret_cast<ulonglong2*>(P.acc + row);
   const ulonglong2 raw = __ldcg(ap);
   __stcg(ap, make_ulonglong2(0ull, 0ull));
@@ -272,19 +275,45 @@ __device__ __forceinline__ void finish_pair(const LaneParams& P, int64_t row, co
   const float2 nf = __ldcg(np);
   if (nf.x != 0.f || nf.y != 0.f) __stcg(np, make_float2(0.f, 0.f));
   const float s0 = nf.x != 0.f ? nf.x : __ll2float_rn((long long)raw.x) * P.fx_inv;
-  store_as<float>(P.y, P.y_dtype, row, (s0 + f.add0) * f.q0);
-  if (row + 1 < P.m) {
-    const float s1 = nf.y != 0.f ? nf.y : __ll2float_rn((long long)raw.y) * P.fx_inv;
-    store_as<float>(P.y, P.y_dtype, row + 1, (s1 + f.add1) * f.q1);
-  }
+  y0 = (s0 + f.add0) * f.q0;
+  const float s1 = nf.y != 0.f ? nf.y : __ll2float_rn((long long)raw.y) * P.fx_inv;
+  y1 = (s1 + f.add1) * f.q1;
+  return true;
 }
 
-__global__ void __launch_bounds__(256) lane_finish_kernel(LaneParams P) {
-  const int64_t row = ((int64_t)blockIdx.x * 256 + threadIdx.x) * 2;
-  const FinishPair f = finish_prefetch(P, row);
+// Eight rows per thread: Y leaves in 16-byte stores (one for fp16 Y, two for
+// fp32) when the rows are all valid and Y is 16-byte aligned -- the form a
+// pinned host Y wants (2-byte stores over PCIe measured slower than a device
+// Y plus a D2H copy) -- else element by element.
+__global__ void __launch_bounds__(128) lane_finish_kernel(LaneParams P) {
+  const int64_t row = ((int64_t)blockIdx.x * 128 + threadIdx.x) * 8;
+  FinishPair f[4];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) f[p] = finish_prefetch(P, row + 2 * p);
   griddep_wait();
   griddep_launch_dependents();
-  finish_pair(P, row, f);
+  float v[8];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) finish_pair_values(P, row + 2 * p, f[p], v[2 * p], v[2 * p + 1]);
+  if (row >= P.m) return;
+  const bool full = row + 8 <= P.m && (reinterpret_cast<uintptr_t>(P.y) & 15) == 0;
+  if (full && P.y_dtype == MSG_F16) {
+    uint32_t w[4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const __half2 h = __floats2half2_rn(v[2 * p], v[2 * p + 1]);
+      w[p] = *reinterpret_cast<const uint32_t*>(&h);
+    }
+    reinterpret_cast<uint4*>(reinterpret_cast<__half*>(P.y) + row)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+  } else if (full && P.y_dtype == MSG_F32) {
+    float4* yp = reinterpret_cast<float4*>(reinterpret_cast<float*>(P.y) + row);
+    yp[0] = make_float4(v[0], v[1], v[2], v[3]);
+    yp[1] = make_float4(v[4], v[5], v[6], v[7]);
+  } else {
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+      if (row + r < P.m) store_as<float>(P.y, P.y_dtype, row + r, v[r]);
+  }
 }
 
 // Work split: the (chunk, 32-row tile) grid linearised chunk-major,
@@ -627,8 +656,8 @@ static int launch_lane_t(LaneParams& P, cudaStream_t s) {
   // the finishing kernel, queued with PDL behind the LUT kernel.  (An in-kernel
   // grid barrier instead measured 2 us slower per call: fence + arrival +
   // release round trips after the last CTA, vs. PDL's overlapped launch.)
-  cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, ceil_div((P.m + 1) / 2, 256)));
-  cfg.blockDim = dim3(256);
+  cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, ceil_div(ceil_div(P.m, 8), 128)));
+  cfg.blockDim = dim3(128);
   cfg.dynamicSmemBytes = 0;
   MSG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, lane_finish_kernel, P));
   return MSG_OK;

@@ -75,6 +75,7 @@ _T2NP = None
 _HOST_Y_DIRECT = __import__("os").environ.get("MSG_HOST_Y", "direct") != "copy"
 
 
+
 def _np_dtype(X):
     global _T2NP
     if _lib.is_torch(X):
@@ -217,10 +218,10 @@ def msgemm(pwm: PackedWeightMatrix, X, d: int, budget: int = DEFAULT_BUDGET,
     return Yh if is_tensor else Yh.numpy()
 
 
-def _host_call(call, Xm, host_out, stream, is_tensor, was_vector):
+def _host_call(call, Xm, host_out, stream, is_tensor, was_vector, pinned=None):
     """Host X in, host Y out through the plan's graph-replayed path."""
     with call.lock:
-        Yh = call.run_host(Xm, host_out, stream)
+        Yh = call.run_host(Xm, host_out, stream, pinned)
         if host_out is not None:
             if Yh is not host_out:
                 host_out.copy_(Yh.reshape(host_out.shape))
@@ -245,6 +246,10 @@ def _register_fast(pwm, X, out, opts, call, stream, dev, is_tensor, was_vector):
     oshape = out.shape if out is not None else None
     optr = out.data_ptr() if out is not None else None
     key = ("fast", id(X), id(out)) + opts
+    # Tensor.is_pinned() asks the driver (cudaPointerGetAttributes, ~4 us per
+    # call): the answer cannot change while the same live tensor keeps the
+    # same data pointer, so the entry remembers it
+    pinned = (bool(is_tensor and X.is_pinned()), bool(out is not None and out.is_pinned()))
 
     def ent(X2, out2):
         if xref() is not X2 or X2.shape != xshape or X2.dtype != xdtype:
@@ -255,7 +260,8 @@ def _register_fast(pwm, X, out, opts, call, stream, dev, is_tensor, was_vector):
             return None
         if _lib.current_stream_handle(dev) != stream or _lib.torch().cuda.current_device() != dev.index:
             return None
-        return _host_call(call, X2[:, None] if was_vector else X2, out2, stream, is_tensor, was_vector)
+        return _host_call(call, X2[:, None] if was_vector else X2, out2, stream, is_tensor, was_vector,
+                          pinned)
 
     cache = pwm._device_cache
     if sum(1 for kk in cache if kk[0] == "fast") >= 8:
@@ -376,7 +382,7 @@ class _CallPlan:
                                                 n, self.b * Y.element_size(),
                                                 _lib.ctypes.c_void_p(Y.data_ptr()), 1, st))
 
-    def run_host(self, Xm, host_out, stream):
+    def run_host(self, Xm, host_out, stream, pinned=None):
         """Host activations in, host Y out (the drop-in call): H2D -> kernels ->
         D2H -> one stream sync.  From the second call with the same host
         buffers on, the three steps replay as one CUDA graph launched and
@@ -392,7 +398,8 @@ class _CallPlan:
             self._xh = xh = t.empty(tuple(Xm.shape), dtype=self.x_dtype, pin_memory=True)
             self._graphs.clear()
         if _lib.is_torch(Xm):
-            if Xm.dtype == self.x_dtype and Xm.is_contiguous() and Xm.is_pinned():
+            if (Xm.dtype == self.x_dtype and Xm.is_contiguous()
+                    and (pinned[0] if pinned is not None else Xm.is_pinned())):
                 src = Xm
             else:
                 src = xh
@@ -401,7 +408,7 @@ class _CallPlan:
             src = xh
             np.copyto(self._xh_np(), Xm, casting="no")
         if (host_out is not None and host_out.dtype == self.y_dtype and host_out.is_contiguous()
-                and host_out.is_pinned()):
+                and (pinned[1] if pinned is not None else host_out.is_pinned())):
             dst = host_out
         else:
             if self._yh is None:
@@ -421,12 +428,16 @@ class _CallPlan:
         return dst
 
     def _launch_to_host(self, dst, stream=None):
-        """Kernels -> Y in host memory.  For b >= 2 the finishing kernels store
-        Y straight into the pinned buffer (device-visible under UVA), so no
-        separate D2H copy trails the kernels (cfg5 e2e 272 -> 263 us); the
-        b = 1 finish writes 2-byte values, which measured faster through a
-        device Y + one D2H copy.  MSG_HOST_Y=copy forces the copy (A/B)."""
-        if _HOST_Y_DIRECT and self.b >= 2:
+        """Kernels -> Y in host memory.  The finishing kernels store Y straight
+        into the pinned buffer (device-visible under UVA) with 16-byte stores,
+        so no separate D2H copy trails the kernels (cfg5 e2e 272 -> 263 us;
+        cfg4 b = 1 36.3 -> 32.8 us, cfg2 34.2 -> 25.7 us once the b = 1 finish
+        wrote eight rows per store -- its former 2-byte stores were slower
+        than a device Y plus one D2H copy).  MSG_HOST_Y=copy forces the copy
+        (A/B).  Reading X in place from the pinned buffer instead of the H2D
+        copy measured no gain when the caller rewrites X between calls (32.8 vs
+        33.2 us, tools/fastpath_profile.py), so the copy node stays."""
+        if _HOST_Y_DIRECT:
             self.launch(self._xs, dst.reshape(self.m, self.b), stream)
         else:
             ys = self.y_stage()

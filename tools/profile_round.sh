@@ -20,6 +20,7 @@ full() {  # config kernel-regex name
 full cfg5 rb_tmem cfg5_rb_tmem16
 full cfg3 rb_tmem cfg3_rb_tmem8
 full cfg4b1 lane_lut cfg4b1_lane_lut
-full cfg4b1 dq_gemv cfg4b1_dq_gemv
+full cfg4b1 dq_hmma cfg4b1_dq_hmma
+full cfg5 dq_hmma cfg5_dq_hmma
 full cfg4b256 dq_mma cfg4b256_dq_mma
 ls -la $O
