@@ -175,6 +175,20 @@ MSG_API int msg_gemm(const uint8_t* packed, const uint8_t* wrep, int64_t m, int6
              void* y, int y_dtype, void* workspace, int64_t workspace_bytes,
              int flags, void* stream);
 
+/* msg_gemm whose finishing kernels store every element of Y also into
+ * n_peers (0..7) more buffers at the same element offset: y_peers[i] is the
+ * address in another rank's Y that corresponds to y (mapped peer memory, e.g.
+ * torch symmetric memory over NVLink; 16-byte aligned like y).  A row-sharded
+ * call (sharded.py) thus leaves its slice in every rank's Y -- the all-gather
+ * of SURVEY.md 8(e) fused into the epilogue; the ranks still need a barrier
+ * before reading.  NOT_SUPPORTED on the generic (global-table) path. */
+MSG_API int msg_gemm_fanout(const uint8_t* packed, const uint8_t* wrep, int64_t m, int64_t k,
+                            int width, const double* values, const void* x, int x_dtype,
+                            int64_t b, int d, int scale_mode, int64_t group_size, const void* q,
+                            int q_dtype, void* y, int y_dtype, void* workspace,
+                            int64_t workspace_bytes, int flags, void* stream,
+                            void* const* y_peers, int n_peers);
+
 /* ---------- K4: dequantise-then-MMA comparison kernel (gemm.py:206-216 naive_gemm) ---------- */
 /* bytes of the tensor-core tile layout of W ([m/128][k/64][128][32 B], nibbles
  * permuted for the fp16 magic-number dequantisation) */

@@ -42,7 +42,7 @@ EXPORTS = (
     "msg_dequant_mma_workspace_bytes", "msg_dequant_mma",
     "msg_mma_layout_bytes", "msg_repack_mma", "msg_row_conditioning", "msg_copy_rows",
     "msg_naive_gemm", "msg_graph_run", "msg_stream_sync", "msg_dequant_gemv",
-    "msg_dequant_hmma",
+    "msg_dequant_hmma", "msg_gemm_fanout",
 )
 
 _c_i64 = ctypes.c_int64
@@ -64,6 +64,9 @@ _SIGS = {
                                _c_i64, _c_int, _vp, _vp, _vp]),
     "msg_gemm": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_int, _vp, _vp, _c_int, _c_i64, _c_int,
                           _c_int, _c_i64, _vp, _c_int, _vp, _c_int, _vp, _c_i64, _c_int, _vp]),
+    "msg_gemm_fanout": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_int, _vp, _vp, _c_int, _c_i64, _c_int,
+                                 _c_int, _c_i64, _vp, _c_int, _vp, _c_int, _vp, _c_i64, _c_int, _vp,
+                                 _vp, _c_int]),
     "msg_dequant_mma_workspace_bytes": (_c_i64, [_c_i64, _c_i64, _c_i64]),
     "msg_dequant_mma": (_c_int, [_vp, _c_i64, _c_i64, _vp, _vp, _c_int, _c_i64, _vp, _c_int,
                                  _vp, _c_i64, _vp]),

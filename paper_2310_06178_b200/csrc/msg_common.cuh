@@ -36,6 +36,17 @@ int max_smem_optin();
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Fan-out of Y (msg_gemm_fanout): every Y store of the finishing kernels is
+// repeated at the same element offset into up to kMaxFan more buffers -- the
+// other ranks' copies of Y, mapped peer memory over NVLink -- so a row-sharded
+// call leaves its slice in every rank's Y without a separate all-gather.
+constexpr int kMaxFan = 7;
+struct YFan {
+  void* p[kMaxFan];
+  int n;
+};
+YFan& current_fan();  // thread-local; empty outside msg_gemm_fanout
+
 inline int row_bytes(int64_t k, int width) {
   // packing.py:39-47 bytes_per_row
   if (width == 4) return (int)((k + 1) / 2);

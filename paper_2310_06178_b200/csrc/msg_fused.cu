@@ -621,7 +621,7 @@ template <int SG>
 __global__ void __launch_bounds__(256) fused_finish_kernel(
     const float* __restrict__ partial, int S, int64_t m, int64_t b, int64_t k, int d,
     const uint16_t* __restrict__ tailp, TailVals vals, const void* x, int x_dtype, int scale_mode,
-    const void* q, int q_dtype, void* y, int y_dtype) {
+    const void* q, int q_dtype, void* y, int y_dtype, YFan fan) {
   constexpr int OPB = 256 / SG;  // outputs per block
   __shared__ float red[SG][OPB];
   const int64_t nb = k / d;
@@ -686,6 +686,7 @@ __global__ void __launch_bounds__(256) fused_finish_kernel(
         if (u < tail) s = fmaf(tw[u], tx[u], s);
       if (scale_mode == MSG_SCALE_PER_ROW) s *= qs;
       store_as<float>(y, y_dtype, t, s);
+      for (int pr = 0; pr < fan.n; ++pr) store_as<float>(fan.p[pr], y_dtype, t, s);
     }
   }
 }
@@ -698,7 +699,7 @@ template <int SG>
 __global__ void __launch_bounds__(256) finish_vec4_kernel(
     const float* __restrict__ partial, int S, int64_t m, int64_t b, int64_t k, int d,
     const uint16_t* __restrict__ tailp, TailVals vals, const void* x, int x_dtype, int scale_mode,
-    const void* q, int q_dtype, void* y, int y_dtype) {
+    const void* q, int q_dtype, void* y, int y_dtype, YFan fan) {
   constexpr int OPB = 256 / SG;  // float4 outputs per block
   __shared__ float4 red[SG > 1 ? SG : 1][OPB];
   const int64_t total = m * b, total4 = total / 4;
@@ -772,18 +773,22 @@ __global__ void __launch_bounds__(256) finish_vec4_kernel(
         *av[e] = r;
       }
     }
-    if (y_dtype == MSG_F16) {
-      __half2 h0 = __floats2half2_rn(a.x, a.y), h1 = __floats2half2_rn(a.z, a.w);
-      *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(y) + t) =
-          make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
-    } else if (y_dtype == MSG_F32) {
-      *reinterpret_cast<float4*>(reinterpret_cast<float*>(y) + t) = a;
-    } else {
-      store_as<float>(y, y_dtype, t, a.x);
-      store_as<float>(y, y_dtype, t + 1, a.y);
-      store_as<float>(y, y_dtype, t + 2, a.z);
-      store_as<float>(y, y_dtype, t + 3, a.w);
-    }
+    auto put = [&](void* yy) {
+      if (y_dtype == MSG_F16) {
+        __half2 h0 = __floats2half2_rn(a.x, a.y), h1 = __floats2half2_rn(a.z, a.w);
+        *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(yy) + t) =
+            make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+      } else if (y_dtype == MSG_F32) {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(yy) + t) = a;
+      } else {
+        store_as<float>(yy, y_dtype, t, a.x);
+        store_as<float>(yy, y_dtype, t + 1, a.y);
+        store_as<float>(yy, y_dtype, t + 2, a.z);
+        store_as<float>(yy, y_dtype, t + 3, a.w);
+      }
+    };
+    put(y);
+    for (int pr = 0; pr < fan.n; ++pr) put(fan.p[pr]);
   }
 }
 
@@ -1047,6 +1052,7 @@ int msg_gemm(const uint8_t* packed, const uint8_t* wrep, int64_t m, int64_t k, i
   cudaStream_t s = as_stream(stream);
   FusedPlan p = fused_plan(m, k, width, values, x_dtype, b, d, scale_mode, group_size, flags);
   if (!p.ok) {
+    if (current_fan().n) return fail(MSG_ERR_UNSUPPORTED, "the generic path has no Y fan-out");
     const CodebookParam cb = make_codebook(values, width);  // 2 KiB block: generic path only
     return run_generic(packed, m, k, width, cb, x, x_dtype, b, d, scale_mode, group_size, q,
                        q_dtype, y, y_dtype, workspace, ws_bytes, s);
@@ -1101,6 +1107,24 @@ int msg_gemm(const uint8_t* packed, const uint8_t* wrep, int64_t m, int64_t k, i
                        y, y_dtype, s);
 }
 
+int msg_gemm_fanout(const uint8_t* packed, const uint8_t* wrep, int64_t m, int64_t k, int width,
+                    const double* values, const void* x, int x_dtype, int64_t b, int d,
+                    int scale_mode, int64_t group_size, const void* q, int q_dtype, void* y,
+                    int y_dtype, void* workspace, int64_t ws_bytes, int flags, void* stream,
+                    void* const* y_peers, int n_peers) {
+  if (n_peers < 0 || n_peers > kMaxFan)
+    return fail(MSG_ERR_VALUE, "fan-out takes 0..%d peer buffers (got %d)", kMaxFan, n_peers);
+  if (n_peers && !y_peers) return fail(MSG_ERR_VALUE, "y_peers is NULL");
+  if (flags & MSG_FLAG_LUT_PHASE_ONLY) n_peers = 0;
+  YFan& fan = current_fan();
+  fan.n = n_peers;
+  for (int i = 0; i < n_peers; ++i) fan.p[i] = y_peers[i];
+  const int e = msg_gemm(packed, wrep, m, k, width, values, x, x_dtype, b, d, scale_mode, group_size,
+                         q, q_dtype, y, y_dtype, workspace, ws_bytes, flags, stream);
+  fan.n = 0;
+  return e;
+}
+
 }  // extern "C"
 
 namespace msg {
@@ -1109,6 +1133,9 @@ int launch_finish(const float* partial, int S, int64_t m, int64_t b, int64_t k, 
                   int scale_mode, const void* q, int q_dtype, void* y, int y_dtype,
                   cudaStream_t s) {
   const int64_t total = m * b;
+  const YFan fan = current_fan();
+  bool fan_aligned = true;  // the vectorised kernel stores 16 / 8 bytes at a time
+  for (int i = 0; i < fan.n; ++i) fan_aligned = fan_aligned && (reinterpret_cast<uintptr_t>(fan.p[i]) & 15) == 0;
   // four outputs per thread group; slices split over SG groups when there are
   // few outputs per SM (e.g. 137 slices x 8192 x 4)
   // (float4 / uint2 stores of Y: a caller-supplied Y must be 16-byte aligned)
@@ -1117,7 +1144,7 @@ int launch_finish(const float* partial, int S, int64_t m, int64_t b, int64_t k, 
   // outputs to fill the GPU: for a GEMV-sized m b the scalar kernel keeps
   // four times more threads busy)
   if (total % 4 == 0 && (b % 4 == 0 || total >= 32768) && scale_mode != MSG_SCALE_PER_GROUP &&
-      S >= 2 && (reinterpret_cast<uintptr_t>(y) & 15) == 0) {
+      S >= 2 && (reinterpret_cast<uintptr_t>(y) & 15) == 0 && fan_aligned) {
     int sg = 1;
     while (sg < 16 && 2 * sg <= S && (total / 4) * sg < (int64_t)sm_count() * 512) sg *= 2;
     const int opb = 256 / sg;
@@ -1133,7 +1160,7 @@ int launch_finish(const float* partial, int S, int64_t m, int64_t b, int64_t k, 
     cfg.numAttrs = 1;
 #define MSG_FIN4(G)                                                                            \
   MSG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, finish_vec4_kernel<G>, partial, S, m, b, k, d, tailp, \
-                                    tv, x, x_dtype, scale_mode, q, q_dtype, y, y_dtype))
+                                    tv, x, x_dtype, scale_mode, q, q_dtype, y, y_dtype, fan))
     switch (sg) {
       case 1: MSG_FIN4(1); break;
       case 2: MSG_FIN4(2); break;
@@ -1164,7 +1191,7 @@ int launch_finish(const float* partial, int S, int64_t m, int64_t b, int64_t k, 
   cfg.numAttrs = 1;
 #define MSG_FIN(G)                                                                            \
   MSG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fused_finish_kernel<G>, partial, S, m, b, k, d,    \
-                                    tailp, tv, x, x_dtype, scale_mode, q, q_dtype, y, y_dtype))
+                                    tailp, tv, x, x_dtype, scale_mode, q, q_dtype, y, y_dtype, fan))
   switch (sg) {
     case 1: MSG_FIN(1); break;
     case 2: MSG_FIN(2); break;

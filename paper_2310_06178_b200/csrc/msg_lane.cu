@@ -160,6 +160,7 @@ struct LaneParams {
   int q_dtype, scale_mode;
   void* y;
   int y_dtype;
+  YFan fan;       // more destinations of Y (msg_gemm_fanout)
   uint32_t ones;    // 0x3C003C00: two fp16 +1.0
   int early;        // MSG_FLAG_STATIC_WEIGHTS: stream weights before griddepcontrol.wait
   int lut_only;     // measurement: the LUT kernel alone (no finish kernel)
@@ -281,39 +282,42 @@ __device__ __forceinline__ bool finish_pair_values(const LaneParams& P, int64_t 
   return true;
 }
 
-// Eight rows per thread: Y leaves in 16-byte stores (one for fp16 Y, two for
-// fp32) when the rows are all valid and Y is 16-byte aligned -- the form a
-// pinned host Y wants (2-byte stores over PCIe measured slower than a device
-// Y plus a D2H copy) -- else element by element.
-__global__ void __launch_bounds__(128) lane_finish_kernel(LaneParams P) {
-  const int64_t row = ((int64_t)blockIdx.x * 128 + threadIdx.x) * 8;
-  FinishPair f[4];
-#pragma unroll
-  for (int p = 0; p < 4; ++p) f[p] = finish_prefetch(P, row + 2 * p);
+// Two rows per thread (as many threads as possible hide the L2 latency of
+// the sums: eight rows per thread measured 1 us slower per call); Y leaves in
+// 16-byte stores assembled with warp shuffles -- four lanes' fp16 pairs, or
+// two lanes' fp32 pairs -- when the rows are valid and Y is 16-byte aligned:
+// the form a pinned host Y wants (2-byte stores over PCIe measured slower
+// than a device Y plus a D2H copy).  Otherwise element by element.
+__global__ void __launch_bounds__(256) lane_finish_kernel(LaneParams P) {
+  const int64_t row = ((int64_t)blockIdx.x * 256 + threadIdx.x) * 2;
+  const int lane = threadIdx.x & 31;
+  const FinishPair f = finish_prefetch(P, row);
   griddep_wait();
   griddep_launch_dependents();
-  float v[8];
-#pragma unroll
-  for (int p = 0; p < 4; ++p) finish_pair_values(P, row + 2 * p, f[p], v[2 * p], v[2 * p + 1]);
-  if (row >= P.m) return;
-  const bool full = row + 8 <= P.m && (reinterpret_cast<uintptr_t>(P.y) & 15) == 0;
-  if (full && P.y_dtype == MSG_F16) {
-    uint32_t w[4];
-#pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      const __half2 h = __floats2half2_rn(v[2 * p], v[2 * p + 1]);
-      w[p] = *reinterpret_cast<const uint32_t*>(&h);
+  float v0, v1;
+  finish_pair_values(P, row, f, v0, v1);
+  const __half2 h = __floats2half2_rn(v0, v1);
+  const uint32_t w0 = *reinterpret_cast<const uint32_t*>(&h);
+  // every lane takes part in the shuffles (rows >= m carry zeros)
+  const uint32_t w1 = __shfl_down_sync(0xffffffffu, w0, 1), w2 = __shfl_down_sync(0xffffffffu, w0, 2),
+                 w3 = __shfl_down_sync(0xffffffffu, w0, 3);
+  const float u0 = __shfl_down_sync(0xffffffffu, v0, 1), u1 = __shfl_down_sync(0xffffffffu, v1, 1);
+  const int64_t row8 = row - 2 * (lane & 3), row4 = row - 2 * (lane & 1);  // first row of the 16-byte store
+  auto put = [&](void* yy) {
+    const bool al = (reinterpret_cast<uintptr_t>(yy) & 15) == 0;
+    if (P.y_dtype == MSG_F16 && al && row8 + 8 <= P.m) {
+      if ((lane & 3) == 0)
+        *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(yy) + row) = make_uint4(w0, w1, w2, w3);
+    } else if (P.y_dtype == MSG_F32 && al && row4 + 4 <= P.m) {
+      if ((lane & 1) == 0)
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(yy) + row) = make_float4(v0, v1, u0, u1);
+    } else {
+      if (row < P.m) store_as<float>(yy, P.y_dtype, row, v0);
+      if (row + 1 < P.m) store_as<float>(yy, P.y_dtype, row + 1, v1);
     }
-    reinterpret_cast<uint4*>(reinterpret_cast<__half*>(P.y) + row)[0] = make_uint4(w[0], w[1], w[2], w[3]);
-  } else if (full && P.y_dtype == MSG_F32) {
-    float4* yp = reinterpret_cast<float4*>(reinterpret_cast<float*>(P.y) + row);
-    yp[0] = make_float4(v[0], v[1], v[2], v[3]);
-    yp[1] = make_float4(v[4], v[5], v[6], v[7]);
-  } else {
-#pragma unroll
-    for (int r = 0; r < 8; ++r)
-      if (row + r < P.m) store_as<float>(P.y, P.y_dtype, row + r, v[r]);
-  }
+  };
+  put(P.y);
+  for (int pr = 0; pr < P.fan.n; ++pr) put(P.fan.p[pr]);
 }
 
 // Work split: the (chunk, 32-row tile) grid linearised chunk-major,
@@ -656,8 +660,8 @@ static int launch_lane_t(LaneParams& P, cudaStream_t s) {
   // the finishing kernel, queued with PDL behind the LUT kernel.  (An in-kernel
   // grid barrier instead measured 2 us slower per call: fence + arrival +
   // release round trips after the last CTA, vs. PDL's overlapped launch.)
-  cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, ceil_div(ceil_div(P.m, 8), 128)));
-  cfg.blockDim = dim3(128);
+  cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, ceil_div((P.m + 1) / 2, 256)));
+  cfg.blockDim = dim3(256);
   cfg.dynamicSmemBytes = 0;
   MSG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, lane_finish_kernel, P));
   return MSG_OK;
@@ -697,6 +701,7 @@ int launch_lane(const uint8_t* wrep, int64_t m, int64_t k, const double* values,
   P.scale_mode = scale_mode;
   P.y = y;
   P.y_dtype = y_dtype;
+  P.fan = current_fan();
   P.ones = 0x3C003C00u;
   P.early = early ? 1 : 0;
   P.lut_only = lut_only ? 1 : 0;

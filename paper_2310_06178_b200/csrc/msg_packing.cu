@@ -19,6 +19,11 @@ static thread_local std::string g_last_error;
 
 void set_error(const std::string& s) { g_last_error = s; }
 
+YFan& current_fan() {
+  static thread_local YFan fan{};
+  return fan;
+}
+
 int fail(int code, const char* fmt, ...) {
   char buf[1024];
   va_list ap;

@@ -125,7 +125,7 @@ def _ensure_device_pwm(pwm):
 
 def msgemm(pwm: PackedWeightMatrix, X, d: int, budget: int = DEFAULT_BUDGET,
            workers: int = 1, *, table_dtype=None, symmetric: bool = True,
-           out_dtype=None, out=None, _flags: int = 0):
+           out_dtype=None, out=None, _flags: int = 0, _fan=None):
     """Two-phase GeMM Y = W @ X on the GPU (gemm.py:89-153).
 
     Returns (m, b), or (m,) for a vector X, in X's dtype.  ``budget`` keeps
@@ -139,6 +139,9 @@ def msgemm(pwm: PackedWeightMatrix, X, d: int, budget: int = DEFAULT_BUDGET,
     out_dtype: None (Y in X's dtype, as the reference) or a float dtype,
         e.g. float32 Y from fp16 X (the bit-exact integer check).
     out: optional preallocated CUDA tensor for Y (torch inputs only).
+    _fan: device addresses (ints, at most 7) of the same Y region in other
+        ranks' buffers (mapped peer memory): the finishing kernels store Y
+        there as well (sharded.msgemm_sharded_fused).  Needs a CUDA ``out``.
     """
     # repeated host-path calls with the same X / out objects (a serving loop
     # reusing its pinned buffers): validation and plan lookup were done on
@@ -190,11 +193,16 @@ def msgemm(pwm: PackedWeightMatrix, X, d: int, budget: int = DEFAULT_BUDGET,
             dev_out = out
         else:
             host_out = out
+    if _fan:
+        if dev_out is None or not on_device:
+            raise ValueError("_fan needs CUDA activations and a CUDA out")
+        if len(_fan) > 7:
+            raise ValueError("at most 7 peer buffers")
     if on_device and host_out is None:  # device in, device out: no staging involved
         xd = call.device_x(Xm)
         Y = dev_out if dev_out is not None else t.empty((m, b), dtype=y_dt, device=dev)
         if m and b:
-            call.launch(xd, Y)
+            call.launch(xd, Y, fan=_fan)
         return Y[:, 0] if (was_vector and dev_out is None) else Y
     # host activations and/or host output: the plan's pinned + device staging
     # buffers are shared by calls on this stream, so one call uses them at a time
@@ -366,21 +374,28 @@ class _CallPlan:
         self._launched = False
         self.lock = threading.Lock()
 
-    def launch(self, xd, Y, stream=None):
+    def launch(self, xd, Y, stream=None, fan=None):
         flags = self._flags if self._launched else self._first_flags
         ws, wsp, wsn = self._ws
         st = self._stream if stream is None else _lib.ctypes.c_void_p(stream)
-        _lib.check(self._fn(*self._args_head, _lib.ctypes.c_void_p(xd.data_ptr()),
-                            *self._args_mid, _lib.ctypes.c_void_p(Y.data_ptr()), self.y_code,
-                            wsp, wsn, flags, st))
+        if fan:   # Y also into the peers' buffers (msg_gemm_fanout)
+            arr = (_lib.ctypes.c_void_p * len(fan))(*[int(a) for a in fan])
+            _lib.check(_lib.lib().msg_gemm_fanout(
+                *self._args_head, _lib.ctypes.c_void_p(xd.data_ptr()), *self._args_mid,
+                _lib.ctypes.c_void_p(Y.data_ptr()), self.y_code, wsp, wsn, flags, st, arr, len(fan)))
+        else:
+            _lib.check(self._fn(*self._args_head, _lib.ctypes.c_void_p(xd.data_ptr()),
+                                *self._args_mid, _lib.ctypes.c_void_p(Y.data_ptr()), self.y_code,
+                                wsp, wsn, flags, st))
         self._launched = True
         if self.fix is not None:   # ill-conditioned rows: full tables, scattered into Y
             sub, rows, n = self.fix
             ys = sub.y_stage()
             sub.launch(xd, ys, stream)
-            _lib.check(_lib.lib().msg_copy_rows(_lib.ctypes.c_void_p(ys.data_ptr()), _lib.ptr(rows),
-                                                n, self.b * Y.element_size(),
-                                                _lib.ctypes.c_void_p(Y.data_ptr()), 1, st))
+            for dst in [Y.data_ptr()] + [int(a) for a in (fan or ())]:
+                _lib.check(_lib.lib().msg_copy_rows(_lib.ctypes.c_void_p(ys.data_ptr()), _lib.ptr(rows),
+                                                    n, self.b * Y.element_size(),
+                                                    _lib.ctypes.c_void_p(dst), 1, st))
 
     def run_host(self, Xm, host_out, stream, pinned=None):
         """Host activations in, host Y out (the drop-in call): H2D -> kernels ->

@@ -90,6 +90,75 @@ def msgemm_sharded(pwm_local: PackedWeightMatrix, X, d: int, m_total: int, group
 
 
 # ----------------------------------------------------------------------------
+# All-gather fused into the epilogue: Y lives in
+# symmetric memory (every rank maps every rank's buffer over NVLink), and the
+# finishing kernels of rank r store its rows straight into all G copies
+# (msg_gemm_fanout) -- no NCCL call, no extra pass over Y; one barrier on the
+# symmetric-memory signal pads before any rank reads.
+# ----------------------------------------------------------------------------
+def peer_targets(buffer_ptrs, rank: int, row_lo: int, row_bytes: int) -> list[int]:
+    """Addresses of row `row_lo` in every OTHER rank's Y buffer (the fan-out
+    destinations of this rank's slice)."""
+    if not 0 <= rank < len(buffer_ptrs):
+        raise ValueError(f"bad rank {rank} of {len(buffer_ptrs)}")
+    if len(buffer_ptrs) > 8:
+        raise ValueError("the fused all-gather fans out to at most 7 peers")
+    return [int(p) + row_lo * row_bytes for r, p in enumerate(buffer_ptrs) if r != rank]
+
+
+class PeerY:
+    """The full Y (m, b) of a row-sharded msGeMM in symmetric memory.
+
+    Needs the NCCL/CUDA symmetric-memory allocator of torch.distributed (one
+    process per GPU, peers on NVLink); raises RuntimeError where that is not
+    available so callers can fall back to `gather_rows`.
+    """
+
+    def __init__(self, m: int, b: int, dtype, device, group=None):
+        import torch.distributed as dist
+        try:
+            import torch.distributed._symmetric_memory as symm
+        except ImportError as e:  # pragma: no cover
+            raise RuntimeError(f"symmetric memory unavailable: {e}") from e
+        self.m, self.b = m, b
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        gname = (group or dist.group.WORLD).group_name
+        try:
+            self.buf = symm.empty((m, b), dtype=dtype, device=device)
+            self.handle = symm.rendezvous(self.buf, gname)
+        except Exception as e:
+            raise RuntimeError(f"symmetric memory rendezvous failed: {e}") from e
+        self.row_bytes = b * self.buf.element_size()
+        self.ptrs = [int(p) for p in self.handle.buffer_ptrs]
+        self.lo, self.hi = shard_bounds(m, self.world, self.rank)
+
+    def local(self):
+        """This rank's rows of its own copy (the `out` of the local msGeMM)."""
+        return self.buf[self.lo:self.hi]
+
+    def targets(self) -> list[int]:
+        return peer_targets(self.ptrs, self.rank, self.lo, self.row_bytes)
+
+    def barrier(self):
+        """Every rank's stores have landed everywhere (on the current stream)."""
+        self.handle.barrier()
+
+
+def msgemm_sharded_fused(pwm_local: PackedWeightMatrix, X, d: int, peer_y: PeerY, **kw):
+    """Y = W @ X for row-sharded W with the all-gather fused into the finishing
+    kernels: returns this rank's full (m, b) Y (a view of symmetric memory,
+    valid until the next call).  X: CUDA tensor (replicated)."""
+    from .gemm import msgemm
+
+    peer_y.barrier()          # nobody still reads the previous call's Y
+    if peer_y.hi > peer_y.lo:
+        msgemm(pwm_local, X, d, out=peer_y.local(), _fan=peer_y.targets(), **kw)
+    peer_y.barrier()
+    return peer_y.buf
+
+
+# ----------------------------------------------------------------------------
 # k-split (SURVEY.md §8(f) row f4): every rank owns a slice of the inner
 # dimension for ALL rows, so the table build is split too (the replicated
 # build is the Amdahl term of row sharding, §8(e)); the exchange is an fp32

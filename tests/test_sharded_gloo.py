@@ -223,3 +223,20 @@ def test_k_split_bounds_align_and_cover():
                     assert all(lo % a == 0 for lo, _ in spans)
     with pytest.raises(ValueError):
         k_split_bounds(10, 3, 2, 2)
+
+
+def test_peer_targets_offsets():
+    """Fan-out destinations of the fused all-gather: every other rank's buffer
+    at this rank's first row (pure address arithmetic, sharded.peer_targets)."""
+    from paper_2310_06178_b200.sharded import peer_targets, shard_bounds
+    ptrs = [0x1000_0000, 0x2000_0000, 0x3000_0000, 0x4000_0000]
+    m, b, item = 1030, 8, 2
+    for r in range(4):
+        lo, _ = shard_bounds(m, 4, r)
+        t = peer_targets(ptrs, r, lo, b * item)
+        assert len(t) == 3 and ptrs[r] + lo * b * item not in t
+        assert t == [p + lo * b * item for i, p in enumerate(ptrs) if i != r]
+    with pytest.raises(ValueError):
+        peer_targets(ptrs, 4, 0, 16)
+    with pytest.raises(ValueError):
+        peer_targets(list(range(9)), 0, 0, 16)
