@@ -222,6 +222,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--gather", default="nccl", choices=["nccl", "peer"],
+                    help="row shards: NCCL all-gather of the Y slices (default), or the all-gather "
+                         "fused into the finishing kernels over symmetric memory (peer stores; "
+                         "opt-in: this pool has no multi-GPU box to measure it on)")
     ap.add_argument("--split", default="rows", choices=["rows", "k"],
                     help="N>1: shard rows (+ all-gather of Y, default) or the inner dimension "
                          "(+ fp32 all-reduce of partial Y; splits the table build too)")
@@ -291,8 +295,17 @@ def main():
                                           codebook=mg.int4_codebook()))
     Yshard = torch.empty((mr, cfg.b), dtype=y_dt, device=dev)
     Yfull = torch.empty((cfg.m, cfg.b), dtype=y_dt, device=dev) if world > 1 else Yshard
+    peer_y = None
+    if world > 1 and not ksplit and not share and args.gather == "peer":
+        from paper_2310_06178_b200.sharded import PeerY
+        peer_y = PeerY(cfg.m, cfg.b, y_dt, dev)       # Y in symmetric memory on every rank
+        Yfull, Yshard = peer_y.buf, peer_y.local()
+        os.environ["MSG_BENCH_NO_GRAPH"] = "1"        # the signal-pad barrier is not captured
 
     def collective():
+        if peer_y is not None:   # the finishing kernels already stored into every rank's Y
+            peer_y.barrier()
+            return
         if share:      # gloo functional test: host-staged collectives
             if ksplit:
                 h = Yshard.cpu()
@@ -314,7 +327,8 @@ def main():
         if flags == TC:
             mg.dequant_gemm(pwms[i % ncopies], xd16, out=Ytc)
             return
-        mg.msgemm(pwms[i % ncopies], xd, cfg.d, out=Yshard, _flags=flags | EXTRA_FLAGS, **kw)
+        fan = peer_y.targets() if (peer_y is not None and not flags and gather) else None
+        mg.msgemm(pwms[i % ncopies], xd, cfg.d, out=Yshard, _flags=flags | EXTRA_FLAGS, _fan=fan, **kw)
         if world > 1 and not flags and gather:
             collective()
 
@@ -504,7 +518,9 @@ def main():
                               + (", 32 bank-private per chunk)" if lane else ")")),
                    "accum": "int64 fixed point across CTAs" if lane else "f32",
                    "y": "fp32" if f32_tables else "fp16",
-                   "parallelism": (f"k-split x{world} + NCCL fp32 all-reduce" if ksplit else
+                   "parallelism": (f"row-shard x{world} + all-gather fused into the finishing kernels "
+                                   "(peer stores over symmetric memory)" if peer_y is not None else
+                                   f"k-split x{world} + NCCL fp32 all-reduce" if ksplit else
                                    f"row-shard x{world}" + (" + NCCL all-gather" if world > 1 else "")),
                    "timing": "CUDA-graph replay of the K steps" if use_graphs else "eager launches",
                    "l2": f"rotate {ncopies} weight copies ({ncopies * shard_bytes / 2**20:.0f} MiB "
