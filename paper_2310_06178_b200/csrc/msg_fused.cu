@@ -32,6 +32,8 @@
 #include <algorithm>
 #include <cstring>
 
+#include <cstdlib>
+
 #include "msg_common.cuh"
 
 namespace msg {
@@ -686,7 +688,11 @@ __global__ void __launch_bounds__(256) fused_finish_kernel(
         if (u < tail) s = fmaf(tw[u], tx[u], s);
       if (scale_mode == MSG_SCALE_PER_ROW) s *= qs;
       store_as<float>(y, y_dtype, t, s);
-      for (int pr = 0; pr < fan.n; ++pr) store_as<float>(fan.p[pr], y_dtype, t, s);
+      if (fan.n) {  // compile-time indices: a dynamic index would move the parameter block to local memory
+#pragma unroll
+        for (int pr = 0; pr < kMaxFan; ++pr)
+          if (pr < fan.n) store_as<float>(fan.p[pr], y_dtype, t, s);
+      }
     }
   }
 }
@@ -788,7 +794,11 @@ __global__ void __launch_bounds__(256) finish_vec4_kernel(
       }
     };
     put(y);
-    for (int pr = 0; pr < fan.n; ++pr) put(fan.p[pr]);
+    if (fan.n) {  // compile-time indices (see fused_finish_kernel)
+#pragma unroll
+      for (int pr = 0; pr < kMaxFan; ++pr)
+        if (pr < fan.n) put(fan.p[pr]);
+    }
   }
 }
 
@@ -1142,8 +1152,14 @@ int launch_finish(const float* partial, int S, int64_t m, int64_t b, int64_t k, 
   // (b % 4 != 0 works as long as m b % 4 == 0: the flat output index is
   // vectorised and every element finds its own row -- worth it with enough
   // outputs to fill the GPU: for a GEMV-sized m b the scalar kernel keeps
-  // four times more threads busy)
-  if (total % 4 == 0 && (b % 4 == 0 || total >= 32768) && scale_mode != MSG_SCALE_PER_GROUP &&
+  // four times more threads busy.  Measured crossover, tools/batch_sweep.py
+  // with MSG_FIN_VEC_MIN: m b = 16384 (8192^2 b = 2) 26.5 -> 22.0 us vectorised,
+  // m b = 12288 (4096^2 b = 3) 15.5 -> 16.8 us: vectorise from 16384 outputs)
+  static const int64_t vec_min = [] {
+    const char* e = std::getenv("MSG_FIN_VEC_MIN");
+    return e ? (int64_t)std::atoll(e) : (int64_t)16384;
+  }();
+  if (total % 4 == 0 && (b % 4 == 0 || total >= vec_min) && scale_mode != MSG_SCALE_PER_GROUP &&
       S >= 2 && (reinterpret_cast<uintptr_t>(y) & 15) == 0 && fan_aligned) {
     int sg = 1;
     while (sg < 16 && 2 * sg <= S && (total / 4) * sg < (int64_t)sm_count() * 512) sg *= 2;

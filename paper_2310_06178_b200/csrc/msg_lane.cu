@@ -317,7 +317,11 @@ __global__ void __launch_bounds__(256) lane_finish_kernel(LaneParams P) {
     }
   };
   put(P.y);
-  for (int pr = 0; pr < P.fan.n; ++pr) put(P.fan.p[pr]);
+  if (P.fan.n) {  // compile-time indices: a dynamic index would move the parameter block to local memory
+#pragma unroll
+    for (int pr = 0; pr < kMaxFan; ++pr)
+      if (pr < P.fan.n) put(P.fan.p[pr]);
+  }
 }
 
 // Work split: the (chunk, 32-row tile) grid linearised chunk-major,
