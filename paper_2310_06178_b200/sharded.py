@@ -6,7 +6,9 @@ the same way across threads).  Rank r of G owns rows
 [r*m/G, (r+1)*m/G) of W, builds the tables for the (replicated) X itself
 and computes its Y slice; the only exchange is one all-gather of the
 row-major Y slices (contiguous in Y), done with torch.distributed (NCCL over
-NVLink/NVSwitch on the GPU box, gloo in the CPU tests).
+NVLink/NVSwitch on the GPU box, gloo in the CPU tests) -- or, opt-in, fused
+into the finishing kernels as peer stores over symmetric memory (PeerY,
+msgemm_sharded_fused below).
 
 Row-chunking is bitwise safe: each row's result depends only on that row's
 weights and X, so the gathered Y equals the single-GPU Y of the same kernel
