@@ -451,6 +451,7 @@ struct RbParams {
   float s[16];            // v[c] - beta
   float beta;
   int rounds_per_slice, nrounds;
+  int rpb;                // rows per CTA of the rounds-of-4 kernel: whole warps (a multiple of 32 RPT), <= 512 RPT
   int early;              // weights may be read before griddepcontrol.wait
   float* partial;         // [S][m][b]
 };
@@ -904,16 +905,19 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_tmem_kernel(RbParams P) {
     const __half2 h2 = __float2half2_rn(P.s[tid]);
     s2h[tid] = *reinterpret_cast<const uint32_t*>(&h2);
   }
-  const int64_t row0 = (int64_t)blockIdx.x * kTmR;
+  // row blocks of P.rpb <= kTmR rows (balanced over the row blocks, whole
+  // warps): warps past the block take part in the builds and barriers only
+  const int64_t row0 = (int64_t)blockIdx.x * P.rpb;
   const int slice = blockIdx.y;
   const int64_t c0 = (int64_t)blockIdx.z * BC;
   const int r_begin = slice * P.rounds_per_slice;
   const int r_end = min(P.nrounds, r_begin + P.rounds_per_slice);
   const int nr = r_end - r_begin;
+  const bool warp_on = warp * 32 * kTmRPT < P.rpb;
   const int64_t my_row = row0 + (int64_t)tid * kTmRPT;
-  const int64_t left = P.m - my_row;
+  const int64_t left = warp_on ? P.m - my_row : 0;
   const int nvalid = left <= 0 ? 0 : (left < kTmRPT ? (int)left : kTmRPT);
-  const bool has_words = my_row < P.mp;
+  const bool has_words = warp_on && my_row < P.mp;
   const uint32_t tab = smem_u32(smem);
 
   if (warp == 0) {
@@ -969,7 +973,7 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_tmem_kernel(RbParams P) {
   __syncthreads();
   tm_fence_after();
   const uint32_t tbase = *tmem_slot + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(warp >> 2) * (8 * kTmRPT);
-  {  // zero accumulators
+  if (warp_on) {  // zero accumulators
     float z[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) z[i] = 0.f;
@@ -1015,6 +1019,7 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_tmem_kernel(RbParams P) {
     }
     MSG_JITTER();
     __syncthreads();
+    if (!warp_on) continue;  // (warp-uniform) no rows of this block: next round's barrier
     // ---- gather: row pairs through registers; the next round's words are
     // loaded into the same registers right after their last use
     const bool more = t + 1 < nr;
@@ -1062,6 +1067,7 @@ __global__ void __launch_bounds__(kRbThreads, 1) rb_tmem_kernel(RbParams P) {
   for (int c = 0; c < BC; ++c) cv[c] = cs[c];
 #pragma unroll
   for (int p = 0; p < kTmRPT / 2; ++p) {
+    if (!warp_on) break;
     float v[16];
     tm_ld16(tbase + 16 * p, v);
     tm_wait_ld();
@@ -1127,7 +1133,7 @@ int rb_repack(const uint8_t* packed, int64_t m, int64_t k, int G, int rpt, uint8
 }
 
 struct RbPlan {
-  int G, bc, S, rps, nrounds, nrow_blocks, ncol_tiles, rpt;
+  int G, bc, S, rps, nrounds, nrow_blocks, ncol_tiles, rpt, rpb;
   int64_t partial_bytes, smem;
 };
 
@@ -1138,7 +1144,15 @@ RbPlan rb_plan(int64_t m, int64_t k, int64_t b, int rpt) {
   p.rpt = p.G == 4 ? rpt : rb_rows_per_thread(p.G);
   RbLayout L = rb_layout(m, k, p.G, p.G == 4 ? rpt : 16);
   p.nrounds = (int)(L.nqp / (p.G / 4));
-  p.nrow_blocks = (int)ceil_div(m, (int64_t)kRbThreads * p.rpt);
+  // rounds of 4: as many row blocks as full-size CTAs need, of equal height in
+  // whole warps (11008 rows at 4096 per CTA: 3 x 3840 instead of 4096 + 4096 +
+  // 2816 -- every CTA gathers for the tallest block)
+  p.rpb = kRbThreads * p.rpt;
+  if (p.G == 4 && m > 0) {
+    const int64_t nrb = ceil_div(m, (int64_t)kRbThreads * p.rpt), wrows = 32 * p.rpt;
+    p.rpb = (int)(ceil_div(ceil_div(m, nrb), wrows) * wrows);
+  }
+  p.nrow_blocks = (int)ceil_div(m, (int64_t)p.rpb);
   p.ncol_tiles = (int)ceil_div(b, p.bc);
   const int64_t base = (int64_t)p.nrow_blocks * p.ncol_tiles;
   int64_t S = std::max<int64_t>(1, sm_count() / std::max<int64_t>(1, base));
@@ -1240,6 +1254,7 @@ int launch_rb(const uint8_t* wrep, int64_t m, int64_t k, const double* values, d
   P.beta = (float)beta;
   P.rounds_per_slice = pl.rps;
   P.nrounds = pl.nrounds;
+  P.rpb = pl.rpb;
   P.early = early ? 1 : 0;
   P.partial = reinterpret_cast<float*>(ws);
   int e = MSG_OK;
