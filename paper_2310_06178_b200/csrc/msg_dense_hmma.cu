@@ -163,6 +163,7 @@ __global__ void __launch_bounds__(kDhThreads, (NT == 1 && kDhDepth <= 2) ? 3 : 2
     auto item_dst = [&](int it, int gg) {  // word (x[k_lo], x[k_lo + 4]) of column gg (n-tile 0)
       const int w = it & 3, j = (it >> 2) & (kDhJ - 1), tt = (it / (4 * kDhJ)) & 3, lc = it / kItemsPerChunk;
       const uint32_t sw = (uint32_t)((gg * 4 + tt) & (kDhJ - 1));
+      MSG_DASSERT(lc >= 0 && lc < kDhSub && gg >= 0 && gg < 8);
       return reinterpret_cast<uint32_t*>(smem + (size_t)lc * NT * kDhTileBytes + (gg * 4 + tt) * kDhLaneBytes +
                                          16 * (j ^ sw) + 4 * w);
     };
@@ -241,6 +242,7 @@ __global__ void __launch_bounds__(kDhThreads, (NT == 1 && kDhDepth <= 2) ? 3 : 2
     for (int c = sub; c < sub_end; c += kDhDepth) {
 #pragma unroll
       for (int u = 0; u < kDhDepth; ++u) {
+        MSG_DASSERT(c + u - sub >= 0 && c + u - sub < kDhSub);
         const uint32_t xb = xs_lane + (uint32_t)((c + u - sub) * NT * kDhTileBytes);
 #pragma unroll
         for (int v = 0; v < kDhNV; ++v) {
@@ -310,6 +312,7 @@ __global__ void __launch_bounds__(kDhThreads, (NT == 1 && kDhDepth <= 2) ? 3 : 2
   for (int i = tid; i < rows_per * NC; i += kDhThreads) {
     const int r = rank * rows_per + i / NC, col = i % NC;
     if (r >= kDhRows) break;
+    MSG_DASSERT(r >= 0 && r < kDhRows && col < NC);
     float sum = 0.f;
     for (int s = 0; s < S; ++s) sum += cl.map_shared_rank(tile, s)[r * NC + col];
     store_y(row0 + r, col, sum);

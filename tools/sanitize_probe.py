@@ -68,5 +68,19 @@ Xh = rng.standard_normal((200, 16)).astype(np.float16)
 pwm = mg.from_codes(rng.integers(0, 16, (256, 200), dtype=np.uint8), cb)
 Yk = mg.dequant_gemm(pwm, torch.from_numpy(Xh).cuda()).cpu().numpy()
 assert orc.rel_error(Yk, orc.dense(pwm.data, 200, 4, orc.int4_values()), Xh) <= 2e-3
+# the weight-streaming dense kernel (mma.sync, cluster split-k over DSMEM): b = 1, 8, 13
+Xh2 = rng.standard_normal((2080, 13)).astype(np.float16)
+pwm2 = mg.from_codes(rng.integers(0, 16, (300, 2080), dtype=np.uint8), cb)
+W2 = orc.dense(pwm2.data, 2080, 4, orc.int4_values())
+for nb in (1, 8, 13):
+    Yh = mg.dequant_gemm(pwm2, torch.from_numpy(np.ascontiguousarray(Xh2[:, :nb])).cuda(), kernel="hmma").cpu().numpy()
+    assert orc.rel_error(Yh, W2, Xh2[:, :nb]) <= 2e-3
+# Y fan-out of the finishing kernels (same-device stand-in peers)
+Xf = torch.from_numpy(rng.standard_normal((700, 8)).astype(np.float16)).cuda()
+pwm3 = mg.from_codes(rng.integers(0, 16, (2100, 700), dtype=np.uint8), cb)
+own = torch.empty((2100, 8), dtype=torch.float16, device="cuda")
+peers = [torch.empty_like(own) for _ in range(2)]
+mg.msgemm(pwm3, Xf, 3, out=own, _fan=[p.data_ptr() for p in peers])
+assert all(torch.equal(p, own) for p in peers)
 torch.cuda.synchronize()
 print("sanitize probe ok")
