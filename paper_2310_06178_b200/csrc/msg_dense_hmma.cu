@@ -387,6 +387,7 @@ extern "C" int msg_dequant_hmma(const uint8_t* packed, int64_t m, int64_t k, con
   if (row_bytes(k, 4) % 16 != 0 || (reinterpret_cast<uintptr_t>(packed) & 15) != 0)
     return fail(MSG_ERR_UNSUPPORTED, "the dense HMMA baseline needs 16-byte aligned rows (k %% 32 == 0)");
   if (m == 0 || k == 0) return MSG_OK;
+  if (k > (int64_t)1 << 30) return fail(MSG_ERR_UNSUPPORTED, "the dense HMMA baseline indexes k with 32 bits");
   DhParams P{};
   P.packed = packed;
   P.m = m;
