@@ -134,6 +134,11 @@ MSG_API int msg_row_conditioning(const uint8_t* packed, int64_t m, int64_t k, in
 
 /* Row gather / scatter of n rows of row_bytes bytes: scatter != 0 ->
  * dst[idx[i]] = src[i]; else dst[i] = src[idx[i]].  idx: device int64 (n,). */
+/* Copy `bytes` from src to dst with a kernel (16-byte aligned; src may be
+ * pinned host memory, read over PCIe under UVA): unlike a memcpy node, the
+ * kernel lets the next kernel of the stream start its prologue (PDL), so the
+ * host path's LUT kernel prefetches weights while X arrives. */
+MSG_API int msg_stage_copy(const void* src, void* dst, int64_t bytes, void* stream);
 MSG_API int msg_copy_rows(const void* src, const int64_t* idx, int64_t n, int64_t row_bytes,
                           void* dst, int scatter, void* stream);
 

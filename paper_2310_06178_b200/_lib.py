@@ -42,7 +42,7 @@ EXPORTS = (
     "msg_dequant_mma_workspace_bytes", "msg_dequant_mma",
     "msg_mma_layout_bytes", "msg_repack_mma", "msg_row_conditioning", "msg_copy_rows",
     "msg_naive_gemm", "msg_graph_run", "msg_stream_sync", "msg_dequant_gemv",
-    "msg_dequant_hmma", "msg_gemm_fanout",
+    "msg_dequant_hmma", "msg_gemm_fanout", "msg_stage_copy",
 )
 
 _c_i64 = ctypes.c_int64
@@ -80,6 +80,7 @@ _SIGS = {
     "msg_graph_run": (_c_int, [_vp, _vp, _c_int]),
     "msg_dequant_gemv": (_c_int, [_vp, _c_i64, _c_i64, _vp, _vp, _c_int, _c_i64, _vp, _c_int, _vp]),
     "msg_dequant_hmma": (_c_int, [_vp, _c_i64, _c_i64, _vp, _vp, _c_int, _c_i64, _vp, _c_int, _vp]),
+    "msg_stage_copy": (_c_int, [_vp, _vp, _c_i64, _vp]),
     "msg_stream_sync": (_c_int, [_vp]),
 }
 

@@ -315,6 +315,30 @@ int msg_row_conditioning(const uint8_t* packed, int64_t m, int64_t k, int d, con
   return MSG_OK;
 }
 
+// src -> dst, 16 bytes per thread (tail bytes by thread 0); lets the next
+// kernel of the stream start its prologue at once (PDL)
+__global__ void __launch_bounds__(256) stage_copy_kernel(const uint8_t* __restrict__ src,
+                                                         uint8_t* __restrict__ dst, int64_t bytes) {
+  griddep_launch_dependents();
+  const int64_t n16 = bytes / 16;
+  for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < n16; i += (int64_t)gridDim.x * 256)
+    reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    for (int64_t i = n16 * 16; i < bytes; ++i) dst[i] = src[i];
+}
+
+int msg_stage_copy(const void* src, void* dst, int64_t bytes, void* stream) {
+  if (bytes < 0) return fail(MSG_ERR_VALUE, "negative size");
+  if (bytes == 0) return MSG_OK;
+  if ((((uintptr_t)src | (uintptr_t)dst) & 15) != 0)
+    return fail(MSG_ERR_VALUE, "msg_stage_copy needs 16-byte aligned buffers");
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(bytes / 16, 256), 2 * sm_count()));
+  stage_copy_kernel<<<grid, 256, 0, as_stream(stream)>>>(static_cast<const uint8_t*>(src),
+                                                        static_cast<uint8_t*>(dst), bytes);
+  MSG_LAUNCH_CHECK();
+  return MSG_OK;
+}
+
 int msg_copy_rows(const void* src, const int64_t* idx, int64_t n, int64_t row_bytes_, void* dst,
                   int scatter, void* stream) {
   if (n < 0 || row_bytes_ < 0) return fail(MSG_ERR_VALUE, "negative row count or size");

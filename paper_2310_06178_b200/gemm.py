@@ -73,6 +73,12 @@ def _check_scales_for_depth(pwm, d: int) -> None:
 
 _T2NP = None
 _HOST_Y_DIRECT = __import__("os").environ.get("MSG_HOST_Y", "direct") != "copy"
+# host X -> device staging inside the replayed graph: a copy kernel
+# (msg_stage_copy) instead of a memcpy node, so the LUT kernel behind it starts
+# under PDL and prefetches weights while X crosses PCIe (bench.py e2e: cfg4
+# b = 1 40.9 -> 27.5 us, cfg2 32.5 -> 23.8 us, cfg5 255 -> 247 us).
+# MSG_HOST_X=memcpy forces the copy node (A/B).
+_HOST_X_KERNEL = __import__("os").environ.get("MSG_HOST_X", "kernel") != "memcpy"
 
 
 
@@ -476,7 +482,12 @@ class _CallPlan:
         g = t.cuda.CUDAGraph()
         with t.cuda.stream(side):
             with t.cuda.graph(g, stream=side, capture_error_mode="thread_local"):
-                self._xs.copy_(src, non_blocking=True)
+                if _HOST_X_KERNEL and src.data_ptr() % 16 == 0:
+                    _lib.check(_lib.lib().msg_stage_copy(
+                        _lib.ctypes.c_void_p(src.data_ptr()), _lib.ctypes.c_void_p(self._xs.data_ptr()),
+                        src.numel() * src.element_size(), _lib.ctypes.c_void_p(side.cuda_stream)))
+                else:
+                    self._xs.copy_(src, non_blocking=True)
                 self._launch_to_host(dst, side.cuda_stream)
         cur.wait_stream(side)
         ex = (g, _lib.ctypes.c_void_p(int(g.raw_cuda_graph_exec())))
