@@ -134,6 +134,12 @@ __global__ void __launch_bounds__(kDhThreads, (NT == 1 && kDhDepth <= 2) ? 3 : 2
   // weights never depend on the preceding kernel: in flight before the PDL wait
 #pragma unroll
   for (int u = 0; u < kDhDepth; ++u) load_w(c_begin + u, wa[u], wb[u]);
+  const int kk = (int)P.k, bb = P.b;
+  if (bb < NT * 8) {  // columns >= b of the staged X are never written: zero them once
+    for (int i = tid; i < kDhSub * NT * kDhTileBytes / 16; i += kDhThreads)
+      reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+  }
   griddep_wait();
   griddep_launch_dependents();
 
@@ -144,7 +150,6 @@ __global__ void __launch_bounds__(kDhThreads, (NT == 1 && kDhDepth <= 2) ? 3 : 2
     for (int i = 0; i < 4; ++i) d[nt][0][i] = d[nt][1][i] = 0.f;
   const uint32_t xs_lane = smem_u32(smem) + (uint32_t)((g * 4 + t) * kDhLaneBytes);
   const bool xvec = (P.b & 7) == 0 && (reinterpret_cast<uintptr_t>(P.x) & 15) == 0;
-  const int kk = (int)P.k, bb = P.b;
 
   for (int sub = c_begin; sub < c_end; sub += kDhSub) {
     const int sub_end = min(c_end, sub + kDhSub);
@@ -152,8 +157,8 @@ __global__ void __launch_bounds__(kDhThreads, (NT == 1 && kDhDepth <= 2) ? 3 : 2
     // ---- stage X rows [kDhChunk sub, kDhChunk sub_end) in B-fragment order:
     // item = (chunk lc, quad lane tt, word group j, word w) holds the
     // activation rows k_lo = kDhChunk c + 8 kDhJ tt + 8 j + w and k_lo + 4 of
-    // every column (columns >= b are never written: their products land in
-    // Y columns that are not stored)
+    // every column (columns >= b hold zeros: their products land in Y columns
+    // that are not stored)
     constexpr int kItemsPerChunk = 4 * kDhJ * 4;
     constexpr int kItems = kDhSub * kItemsPerChunk / kDhThreads;
     const int nit = (sub_end - sub) * kItemsPerChunk;
