@@ -1159,10 +1159,15 @@ int launch_finish(const float* partial, int S, int64_t m, int64_t b, int64_t k, 
     const char* e = std::getenv("MSG_FIN_VEC_MIN");
     return e ? (int64_t)std::atoll(e) : (int64_t)16384;
   }();
-  if (total % 4 == 0 && (b % 4 == 0 || total >= vec_min) && scale_mode != MSG_SCALE_PER_GROUP &&
-      S >= 2 && (reinterpret_cast<uintptr_t>(y) & 15) == 0 && fan_aligned) {
-    int sg = 1;
-    while (sg < 16 && 2 * sg <= S && (total / 4) * sg < (int64_t)sm_count() * 512) sg *= 2;
+  // the slice-group count fixes the fp32 summation order: a shape the
+  // vectorised kernel can take uses ITS count in the scalar kernel too, so Y
+  // does not depend on where the caller's buffer happens to be aligned
+  const bool vec_shape = total % 4 == 0 && (b % 4 == 0 || total >= vec_min) &&
+                         scale_mode != MSG_SCALE_PER_GROUP && S >= 2;
+  int sg_vec = 1;
+  while (sg_vec < 16 && 2 * sg_vec <= S && (total / 4) * sg_vec < (int64_t)sm_count() * 512) sg_vec *= 2;
+  if (vec_shape && (reinterpret_cast<uintptr_t>(y) & 15) == 0 && fan_aligned) {
+    const int sg = sg_vec;
     const int opb = 256 / sg;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)std::max<int64_t>(
@@ -1190,6 +1195,7 @@ int launch_finish(const float* partial, int S, int64_t m, int64_t b, int64_t k, 
   // slice groups per output: enough loads in flight to cover the SMs
   int sg = 1;
   while (sg < 32 && 2 * sg <= S && total * sg < (int64_t)sm_count() * 2048) sg *= 2;
+  if (vec_shape) sg = sg_vec;
   const int opb = 256 / sg;
   const int grid =
       (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, opb), (int64_t)sm_count() * 16));

@@ -131,3 +131,28 @@ def test_foreign_weight_objects_are_wrapped_once():
     assert y1.tobytes() == y2.tobytes()
     W = orc.int4_values()[codes] * q[:, None]
     assert orc.rel_error(y1.astype(np.float64), W, X) <= 2e-3
+
+
+@pytest.mark.parametrize("b", [1, 8])
+def test_misaligned_pinned_buffers(b, monkeypatch):
+    """Pinned views that start off a 16-byte boundary: X then goes through a
+    memcpy node instead of the copy kernel (msg_stage_copy), Y through the
+    element-wise stores -- same bits as the device path, on every replay."""
+    import torch
+    rng = np.random.default_rng(40 + b)
+    m, k = 1000, 600
+    pwm = mg.from_codes(rng.integers(0, 16, (m, k), dtype=np.uint8), mg.int4_codebook())
+    xbig = torch.empty(k * b + 8, dtype=torch.float16).pin_memory()
+    ybig = torch.empty(m * b + 8, dtype=torch.float16).pin_memory()
+    for xo, yo in ((1, 0), (0, 3), (5, 1)):
+        xpin = xbig[xo:xo + k * b].reshape(k, b)
+        ypin = ybig[yo:yo + m * b].reshape(m, b)
+        assert xpin.is_pinned() and ypin.is_pinned()
+        for _ in range(4):
+            X = rng.standard_normal((k, b)).astype(np.float16)
+            xpin.copy_(torch.from_numpy(X))
+            ybig.fill_(9)
+            y = mg.msgemm(pwm, xpin, 3, out=ypin)
+            assert y is ypin
+            assert np.array_equal(ypin.numpy().view(np.uint16), _device_ref(pwm, X, 3).reshape(m, b).view(np.uint16))
+            assert bool((ybig[:yo] == 9).all()) and bool((ybig[yo + m * b:] == 9).all())
