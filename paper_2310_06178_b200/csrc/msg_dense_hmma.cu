@@ -51,7 +51,10 @@ constexpr int kDhChunk = 128 * kDhNV;   // weights per (row, warp iteration): a 
 #define MSG_DH_DEPTH 4
 #endif
 constexpr int kDhDepth = MSG_DH_DEPTH;  // chunks in flight per warp
-constexpr int kDhSubK = 2048;           // activation rows per staged X sub-slice
+#ifndef MSG_DH_SUBK
+#define MSG_DH_SUBK 2048
+#endif
+constexpr int kDhSubK = MSG_DH_SUBK;    // activation rows per staged X sub-slice
 constexpr int kDhSub = kDhSubK / kDhChunk;
 static_assert(kDhSub % kDhDepth == 0, "sub-slices hold whole pipeline rounds");
 
