@@ -16,7 +16,7 @@ from oracle import msgemm_oracle as orc  # noqa: E402
 budget = float(sys.argv[1]) if len(sys.argv) > 1 else 120.0
 rng = np.random.default_rng(int(os.environ.get("SOAK_SEED", "7")))
 t0 = time.time()
-n = {"hmma": 0, "lane": 0, "fan": 0}
+n = {"hmma": 0, "lane": 0, "fan": 0, "host": 0}
 while time.time() - t0 < budget:
     # ---- dense HMMA kernel: integer X bit-exact against numpy
     m = int(rng.integers(1, 3000)); k = 32 * int(rng.integers(1, 200)); b = int(rng.integers(1, 17))
@@ -78,4 +78,17 @@ while time.time() - t0 < budget:
         assert torch.equal(bufr, own), ("fan", m, k, b)
     assert bool((own[0] == 5).all()) and bool((own[m + 1] == 5).all())
     n["fan"] += 1
+    # ---- host path (numpy in / numpy out, graph replays from the 2nd call) vs the device path
+    os.environ.pop("MSG_DH_SPLIT", None)
+    m = int(rng.integers(1, 2000)); k = int(rng.integers(3, 1200)); b = int(rng.choice([1, 1, 2, 3, 4, 8, 13]))
+    codes = rng.integers(0, 16, (m, k), dtype=np.uint8)
+    if rng.random() < 0.3:
+        codes[::7] = 0
+    pwm = mg.from_codes(codes, mg.int4_codebook())
+    for _ in range(3):
+        Xn = rng.standard_normal((k, b)).astype(np.float16)
+        yh = mg.msgemm(pwm, Xn, 3)
+        yd = mg.msgemm(pwm, torch.from_numpy(Xn).cuda(), 3).cpu().numpy()
+        assert yh.shape == (m, b) and np.array_equal(yh.view(np.uint16), yd.view(np.uint16)), ("host", m, k, b)
+    n["host"] += 1
 print("soak ok", n, f"{time.time() - t0:.0f}s")
