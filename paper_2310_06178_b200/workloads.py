@@ -37,6 +37,9 @@ CONFIGS = {
     "cfg4b64": Config("cfg4b64", 8192, 8192, 64, 3, "float16", 4, "batch sweep"),
     "cfg4b256": Config("cfg4b256", 8192, 8192, 256, 3, "float16", 4, "batch sweep"),
     "cfg5": Config("cfg5", 65536, 8192, 8, 3, "float16", 5, "row-sharded large GEMM"),
+    # not a BASELINE config: the cfg5 matrix as a GEMV -- a b = 1 kernel long enough
+    # (268 MB of weights) for launch ramp and drain not to set its HBM fraction
+    "cfg5b1": Config("cfg5b1", 65536, 8192, 1, 3, "float16", 5, "extra: cfg5's matrix at b = 1"),
 }
 
 

@@ -9,7 +9,7 @@ import sys
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
-ORDER = ["cfg1", "cfg2", "cfg2int", "cfg3", "cfg4b1", "cfg4b4", "cfg4b16", "cfg4b64", "cfg4b256",
+ORDER = ["cfg1", "cfg2", "cfg2int", "cfg3", "cfg4b1", "cfg4b4", "cfg4b16", "cfg4b64", "cfg4b256", "cfg5b1",
          "cfg5"]
 
 
