@@ -43,7 +43,7 @@ def _dense_check(data, m, k, X, Y, tol, exact):
 
 
 @pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg2int", "cfg3", "cfg4b1", "cfg4b4",
-                                  "cfg4b16", "cfg4b64", "cfg4b256", "cfg5"])
+                                  "cfg4b16", "cfg4b64", "cfg4b256", "cfg5", "cfg5b1"])
 def test_config_parity(name):
     cfg = CONFIGS[name]
     data = weights(cfg)
